@@ -1,0 +1,256 @@
+"""Pins for the C oracle (oracle/nseries_oracle.c via oracle/oracle.py).
+
+C-1 (series_sum) is pinned against closed forms, exact rational brute force and
+the paper's printed Table 3 residuals; C-2 (plan_apply) against C-1 for exact
+plans, against exact inverses for nilpotent matrices (prefix law, Lemma 5), and
+against an independent mpmath matrix-level evaluation of the paper's circuit
+iteration.
+"""
+import math
+from fractions import Fraction as F
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+from oracle import kernels as K
+from oracle import oracle as O
+from paper_2602_11843_b200 import inputs
+
+LD = np.longdouble
+
+
+def _frac_matmul(X, Y):
+    n = len(X)
+    return [[sum(X[i][t] * Y[t][j] for t in range(n)) for j in range(n)] for i in range(n)]
+
+
+def _frac_inverse_unit_upper(Mx):
+    """Inverse of a unit upper-triangular rational matrix by back substitution."""
+    n = len(Mx)
+    inv = [[F(0)] * n for _ in range(n)]
+    for col in range(n):
+        for i in range(n - 1, -1, -1):
+            s = F(1) if i == col else F(0)
+            for t in range(i + 1, n):
+                s -= Mx[i][t] * inv[t][col]
+            inv[i][col] = s / Mx[i][i]
+    return inv
+
+
+def test_k1_is_identity(oracle_lib):
+    A = inputs.random_matrix(7, 1)
+    S = O.full_series(A, 1)
+    assert np.array_equal(S, np.eye(7, dtype=LD))
+
+
+def test_diagonal_closed_form(oracle_lib):
+    # diagonal A: S_k = diag((1 - a^k) / (1 - a)) -- geometric series
+    rng = np.random.default_rng(11)
+    a = rng.uniform(-0.95, 0.95, 9)
+    k = 37
+    S = O.full_series(np.diag(a), k)
+    for i, ai in enumerate(a):
+        fa = F(float(ai))
+        exact = (1 - fa ** k) / (1 - fa)
+        assert abs(F(str(S[i, i])) - exact) <= abs(exact) * F(1, 10 ** 17)
+    assert np.count_nonzero(S - np.diag(np.diag(S))) == 0
+
+
+def test_nilpotent_equals_inverse(oracle_lib):
+    # strictly upper triangular A (A^d = 0): S_k = (I - A)^{-1} exactly for k >= d
+    d = 9
+    rng = np.random.default_rng(5)
+    A = np.triu(rng.integers(-4, 5, (d, d)) / 8.0, 1)
+    I_minus_A = [[F(int(i == j)) - F(float(A[i, j])) for j in range(d)] for i in range(d)]
+    inv = _frac_inverse_unit_upper(I_minus_A)
+    for k in (d, d + 5):
+        S = O.full_series(A, k)
+        for i in range(d):
+            for j in range(d):
+                assert F(str(S[i, j])) == inv[i][j] or abs(F(str(S[i, j])) - inv[i][j]) < F(1, 10 ** 15)
+    # and for k < d the truncated sum differs exactly by the missing powers
+    S3 = O.full_series(A, 3)
+    A_f = [[F(float(x)) for x in row] for row in A]
+    A2 = _frac_matmul(A_f, A_f)
+    for i in range(d):
+        for j in range(d):
+            assert F(str(S3[i, j])) == F(int(i == j)) + A_f[i][j] + A2[i][j]
+
+
+def test_rational_bruteforce(oracle_lib):
+    # brute force over Q at d <= 8: S_k = sum_j A^j with exact Fraction matrix powers
+    d, k = 5, 13
+    rng = np.random.default_rng(3)
+    A = rng.integers(-3, 4, (d, d)) / 16.0
+    Af = [[F(float(x)) for x in row] for row in A]
+    acc = [[F(int(i == j)) for j in range(d)] for i in range(d)]
+    P = [row[:] for row in acc]
+    for _ in range(k - 1):
+        P = _frac_matmul(P, Af)
+        acc = [[acc[i][j] + P[i][j] for j in range(d)] for i in range(d)]
+    S = O.full_series(A, k)
+    for i in range(d):
+        for j in range(d):
+            ex = acc[i][j]
+            assert abs(F(str(S[i, j])) - ex) <= F(1, 10 ** 16) * (1 + abs(ex))
+
+
+def test_telescoped_closed_form(oracle_lib):
+    # (I - A) S_k = I - A^k  (telescoping identity) at small d, long double
+    d, k = 20, 31
+    A = inputs.random_matrix(d, 21, 0.7)
+    S = O.full_series(A, k)
+    lhs = S - O.matvec(A, S)
+    Ak = np.eye(d, dtype=LD)
+    for _ in range(k):
+        Ak = O.matvec(A, Ak)
+    rhs = np.eye(d, dtype=LD) - Ak
+    assert O.rel_fro(lhs, rhs) < 1e-16
+
+
+def test_probe_mode_matches_full(oracle_lib):
+    d, k = 30, 17
+    A = inputs.random_matrix(d, 4)
+    V, idx = inputs.probe_block(d, 4)
+    Sfull = O.full_series(A, k)
+    SV, used = O.series_sum(A, k, V)
+    assert used == k
+    ref = O.matvec(np.asarray(Sfull, dtype=np.float64), V)  # rounding S to f64 -> loose bound
+    assert O.rel_fro(SV, ref) < 1e-15
+
+
+def test_rigorous_early_stop(oracle_lib):
+    d = 40
+    A = inputs.random_matrix(d, 9, 0.3)
+    q = float(np.linalg.norm(A, 2)) * (1 + 1e-12)
+    V, _ = inputs.probe_block(d, 9, 4, 4)
+    full, used_full = O.series_sum(A, 5000, V)
+    early, used = O.series_sum(A, 5000, V, norm_bound=q, tail_tol=1e-19)
+    assert used < 200 and used_full == 5000
+    assert O.rel_fro(early, full) < 1e-18
+
+
+@pytest.mark.parametrize("k,printed", [(81, 4.0e-4), (125, 3.4e-6), (128, 2.5e-6)])
+def test_table3_normal_residuals(oracle_lib, k, printed):
+    # PAPER.md:747-751 (Table 3): ||I - (I-A) S_k||_F at d=500, rho(A)=0.9, normal A,
+    # D = linspace(-1,1,d) (reading R13).  Printed to 2 significant digits.
+    A, Om, D = inputs.table3_matrix()
+    S = O.full_series(A, k)
+    R = np.eye(500, dtype=LD) - S + O.matvec(A, S)
+    res = float(np.sqrt(np.sum(R * R)))
+    assert float(f"{res:.1e}") == printed
+
+
+# ---------------------------------------------------------------- C-2
+
+
+@pytest.mark.parametrize("steps", [[9, 9], [5, 5, 5], [2] * 6, [5, 1, 9], [1, 2, 1, 5], [9, 1, 2]])
+def test_plan_exact_equals_series(oracle_lib, steps):
+    # exact kernels: the plan polynomial is S_k (block concatenation + telescoping)
+    d = 24
+    A = inputs.random_matrix(d, 2, 0.6)
+    V, _ = inputs.probe_block(d, 2, 2, 2)
+    from oracle.plan import plan_reaches
+    k = plan_reaches(steps)
+    Y, R = O.plan_apply(A, steps, V, want_R=True)
+    SV, _ = O.series_sum(A, k, V)
+    assert O.rel_fro(Y, SV) < 1e-17
+    # exact plans: R = A^k (Lemma 5 with E(z) = z^m).  The paper form
+    # R = I - (I-A)Y cancels O(||Y||) terms, so compare against ||Y|| (absolute scale).
+    W = V.astype(LD)
+    for _ in range(k):
+        W = O.matvec(A, W)
+    assert float(np.sqrt(np.sum((R - W) ** 2)) / np.sqrt(np.sum(Y ** 2))) < 1e-17
+
+
+def _nilpotent(d, seed):
+    rng = np.random.default_rng(seed)
+    return np.triu(rng.integers(-2, 3, (d, d)) / 4.0, 1)
+
+
+@pytest.mark.parametrize("steps,d", [([15], 12), ([15], 15), ([15, 15], 40), ([15, 1, 5], 60)])
+def test_plan_prefix_nilpotent(oracle_lib, steps, d):
+    # Lemma 5(3): Y_n = sum_{j < m^n} A^j + O(A^{m^n}).  With A^d = 0 and
+    # d <= prefix length, Y_n = (I - A)^{-1} up to the binary64 prefix error of f.
+    A = _nilpotent(d, d)
+    V, _ = inputs.probe_block(d, 1, 2, 2)
+    Y = O.plan_apply(A, steps, V)
+    X, _ = O.series_sum(A, d, V)                     # = (I - A)^{-1} V exactly (A^d = 0)
+    assert O.rel_fro(Y, X) < 1e-13
+
+
+def test_plan_prefix_breaks_past_prefix(oracle_lib):
+    # radix-15 has spillover: with nilpotency index 17 > 15 the one-step result is NOT (I-A)^{-1}
+    d = 17
+    A = np.diag(np.ones(d - 1), 1) * 0.5
+    V = np.eye(d)[:, :1] * 0 + np.eye(d)[:, -1:]
+    Y = O.plan_apply(A, [15], V)
+    X, _ = O.series_sum(A, d, V)
+    f = K.kernel_coeffs(15)
+    # column d-1 of f(A): entry (0, d-1) picks [f]_{16} 0.5^16 vs exact 0.5^16
+    assert abs(float(Y[0, 0]) - float(f[16]) * 0.5 ** 16) < 1e-18
+    assert abs(float(X[0, 0]) - 0.5 ** 16) < 1e-18
+
+
+def _mp_circuit_iteration(A, steps, params, dps=40):
+    """Paper's Eq. generalradix with f evaluated by its CIRCUIT (Eq. factors, radix15kernel),
+    matrix-level in mpmath -- an independent formulation of what C-2 computes."""
+    mp.mp.dps = dps
+    d = A.shape[0]
+    Am = mp.matrix([[mp.mpf(float(x)) for x in row] for row in A])
+    I = mp.eye(d)
+    Y, R = I, Am
+
+    def lc(w, basis):
+        out = mp.zeros(d, d)
+        for wi, X in zip(w, basis):
+            out += mp.mpf(wi) * X
+        return out
+
+    for s in steps:
+        if s == 1:
+            Y, R = Y + R, Am * R
+            continue
+        assert s == 15
+        P1 = R * R
+        basis = [I, R, P1]
+        P2 = lc(params["L2"], basis) * lc(params["R2"], basis)
+        basis.append(P2)
+        P3 = lc(params["L3"], basis) * lc(params["R3"], basis)
+        basis.append(P3)
+        P4 = lc(params["L4"], basis) * lc(params["R4"], basis)
+        g = params["gamma"]
+        f = I + g[0] * R + g[1] * P1 + g[2] * P2 + g[3] * P3 + P4
+        Y = Y * f
+        R = I - (I - Am) * Y
+    return Y, R
+
+
+@pytest.mark.parametrize("steps", [[15], [15, 15], [15, 1, 15]])
+def test_plan_radix15_vs_mpmath_circuit(oracle_lib, steps):
+    d = 4
+    A = inputs.random_matrix(d, 77, 0.8)
+    params = K.polished_radix15_binary64()
+    Ym, Rm = _mp_circuit_iteration(A, steps, params)
+    V = np.eye(d)
+    Y, R = O.plan_apply(A, steps, V, want_R=True)
+    Ymn = np.array([[float(Ym[i, j]) for j in range(d)] for i in range(d)], dtype=LD)
+    Rmn = np.array([[float(Rm[i, j]) for j in range(d)] for i in range(d)], dtype=LD)
+    assert O.rel_fro(Y, Ymn) < 1e-15
+    scale = max(float(np.sqrt(np.sum(Rmn ** 2))), float(np.sqrt(np.sum(Ymn ** 2))))
+    assert float(np.sqrt(np.sum((R - Rmn) ** 2))) / scale < 1e-15
+
+
+def test_plan_radix15_deviation_from_series(oracle_lib):
+    # F3: an approximate plan computes Y_n = M^{-1}(I - R_n), not S_k; (I-A)(Y - S_k) = A^k - R_n
+    d = 16
+    A = inputs.random_matrix(d, 8, 0.9)
+    V, _ = inputs.probe_block(d, 8, 2, 2)
+    Y, R = O.plan_apply(A, [15, 15], V, want_R=True)
+    S, _ = O.series_sum(A, 225, V)
+    W = V.astype(LD)
+    for _ in range(225):
+        W = O.matvec(A, W)
+    lhs = (Y - S) - O.matvec(A, np.asarray(Y - S, dtype=np.float64))
+    assert O.rel_fro(lhs, W - R) < 1e-6
