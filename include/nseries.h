@@ -1,0 +1,179 @@
+/*
+ * nseries.h -- C ABI of the B200-native truncated-Neumann-series library
+ * (arXiv 2602.11843, "radix kernels").  sm_100a only.
+ *
+ * Problem (Eq. series): given A in R^{d x d} and k >= 1,
+ * return S_k(A) = I + A + ... + A^{k-1}.  Cost is counted in d x d matrix
+ * products.  S_k is reached by radix-kernel splitting
+ * S_{mn}(A) = S_n(A) T_m(A^n) (Eq. decomposition) with
+ *   - binary splitting (m=2),
+ *   - the radix-5 kernel,
+ *   - the exact 3-product radix-9 kernel (Theorem 1),
+ *   - the approximate 4-product radix-15 kernel
+ *     inside the residual framework Y_{n+1} = Y_n f(R_n), R_{n+1} = I - M Y_{n+1}
+ *     (PAPER.md:551-558),
+ *   - "+1" steps S_{n+1} = S_n + A^n for arbitrary k (no paper counterpart;
+ *     DESIGN.md reading R5),
+ * composed into plans by a fewest-product plan builder.
+ *
+ * Conventions for every entry point:
+ *   - Matrices are dense, row-major, contiguous, leading dimension d.
+ *   - Pointers named A, S, R_out, X, Y, C are DEVICE pointers (cudaMalloc /
+ *     torch CUDA tensors) unless the function name ends in _host.
+ *   - The caller owns A, S, R_out; the library owns its workspace (allocated
+ *     lazily per handle, freed by nseries_destroy).  A is read-only and must
+ *     not alias S or R_out.
+ *   - Work is enqueued asynchronously on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  Argument errors are returned
+ *     synchronously before anything is enqueued.  CUDA errors are returned as
+ *     NSERIES_ERR_CUDA and are sticky for the handle.
+ *   - A handle is not thread-safe; use one handle per host thread / stream.
+ *   - There is no CPU fallback: every arithmetic step runs in this library's
+ *     sm_100a kernels; without a usable sm_100a device, create() fails.
+ */
+#ifndef NSERIES_H
+#define NSERIES_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nseries_ctx* nseries_handle;
+
+typedef enum {
+  NSERIES_OK = 0,
+  NSERIES_ERR_INVALID_ARG = 1,      /* bad pointer / size / flag combination          */
+  NSERIES_ERR_UNSUPPORTED_RADIX = 2,/* radix outside {2,5,9,15} (or "+1" = 1)         */
+  NSERIES_ERR_PLAN_K_MISMATCH = 3,  /* plan does not reach k (pure plan with k!=m^t) */
+  NSERIES_ERR_APPROX_TELESCOPE = 4, /* approximate kernel in a telescoping-form step,
+                                       or approximate radix without ALLOW_APPROX      */
+  NSERIES_ERR_ALIAS = 5,            /* A aliases S or R_out                          */
+  NSERIES_ERR_OOM = 6,              /* workspace allocation failed                   */
+  NSERIES_ERR_CUDA = 7,             /* CUDA runtime / launch error (sticky)          */
+  NSERIES_ERR_NO_DEVICE = 8,        /* no sm_100 device                              */
+  NSERIES_ERR_UNSUPPORTED_SIZE = 9  /* e.g. batched path with d > 64                 */
+} nseries_status;
+
+typedef enum {
+  NSERIES_F64 = 0, /* IEEE binary64 throughout; FP64 tensor cores (DMMA)               */
+  NSERIES_F32 = 1  /* fp32 in/out; products as 3xTF32 on tcgen05 with fp32 accumulate  */
+} nseries_dtype;
+
+typedef enum {
+  NSERIES_PLAN_AUTO = 0,     /* fewest products over the radix set (default {9,5,2},
+                                {15,9,5,2} with NSERIES_ALLOW_APPROX)                 */
+  NSERIES_PLAN_BINARY = 2,   /* pure plans: k must equal m^t          */
+  NSERIES_PLAN_RADIX5 = 5,
+  NSERIES_PLAN_RADIX9 = 9,
+  NSERIES_PLAN_RADIX15 = 15,
+  NSERIES_PLAN_CUSTOM = -1   /* caller fills nseries_plan.step[] itself               */
+} nseries_plan_kind;
+
+/* flags (bitwise OR) */
+#define NSERIES_ELIDE_TRIVIAL    0x1u /* skip the S_1 = I concatenation and the unused final
+                                         power/residual product; default is the
+                                         paper's counting (mu_m + 2) t of Table 2            */
+#define NSERIES_ALLOW_APPROX     0x2u /* allow the approximate radix-15 kernel (residual form) */
+#define NSERIES_RFORM_TELESCOPE  0x4u /* radix-15 residual update as R' = I - f + f R instead
+                                         of the paper's R' = I - M Y' (PAPER.md:557 vs 573)   */
+#define NSERIES_NO_GRAPH         0x8u /* do not capture/replay the op list as a CUDA graph     */
+#define NSERIES_SYNC_STATS       0x10u/* record per-op CUDA events for nseries_last_stats      */
+
+#define NSERIES_MAX_STEPS 128
+
+/* A plan: a sequence of steps from n = 1 to n = k.  step[i] = m in {2,5,9,15}
+ * multiplies n by m; step[i] = 1 is a "+1" step.  form[i] is filled by the
+ * builder: 0 = telescoping power update R' = I - T + T R (exact kernels,
+ * PAPER.md:211-212), 1 = paper residual update R' = I - M Y',
+ * 2 = telescoping-form residual R' = I - f + f R.  products = GEMMs executed
+ * under `flags`.  approx = 1 if any step is radix 15 (then the result is the
+ * residual-framework polynomial Y_n, which agrees with S_k on degrees < k;
+ * Y_n - S_k = M^{-1}(A^k - R_n)). */
+typedef struct {
+  int32_t n_steps;
+  int32_t step[NSERIES_MAX_STEPS];
+  int32_t form[NSERIES_MAX_STEPS];
+  int32_t products;
+  int32_t approx;
+  uint32_t flags;
+  int64_t k;
+} nseries_plan;
+
+typedef struct {
+  int32_t products;        /* GEMMs launched by the last eval (== plan.products)            */
+  int32_t launches;        /* all kernel launches of the last eval (GEMMs + degenerate ops)  */
+  int32_t graph_replayed;  /* 1 if the last eval replayed a cached CUDA graph                */
+  int32_t n_ops;
+  float   ms_total;        /* device time of the last eval (NSERIES_SYNC_STATS only, else 0) */
+} nseries_stats;
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+/* Create a handle bound to CUDA device `device`.  Fails with NSERIES_ERR_NO_DEVICE if the
+ * device is not sm_100 (the only architecture the kernels are built for). */
+nseries_status nseries_create(nseries_handle* h, int device);
+nseries_status nseries_destroy(nseries_handle h);
+const char*    nseries_status_string(nseries_status s);
+/* Version string of the library build (arch, git-independent). */
+const char*    nseries_version(void);
+
+/* ---- host-only plan builder (no device needed) ----------------------------------------
+ * Pure kinds require k = m^t.  AUTO searches plans over `radices` (NULL -> default set) for
+ * the fewest products, tie-break: fewest "+1", fewest steps, larger radices first
+ * (reading R6).  Returns NSERIES_ERR_PLAN_K_MISMATCH / _UNSUPPORTED_RADIX /
+ * _APPROX_TELESCOPE on invalid requests.  k in [1, 2^62]. */
+nseries_status nseries_plan_build(int64_t k, nseries_plan_kind kind, const int32_t* radices,
+                                  int32_t n_radices, uint32_t flags, nseries_plan* out);
+/* Validate a CUSTOM plan (steps filled by caller), fill form/products/approx/k. */
+nseries_status nseries_plan_finalize(nseries_plan* plan, int64_t k, uint32_t flags);
+
+/* Monomial coefficients [f]_0..[f]_D of the radix-m kernel polynomial as this library
+ * evaluates it (binary64 circuit parameters).  coeffs may be NULL to query
+ * the count; *n_coeffs in: capacity, out: D+1.  mu = products of the circuit. */
+nseries_status nseries_kernel_info(int32_t m, int32_t* mu, int32_t* exact, double* coeffs,
+                                   int32_t* n_coeffs);
+
+/* ---- evaluation -----------------------------------------------------------------------
+ * S <- S_k(A) (exact plans) or the plan polynomial Y_n (approximate plans), d x d, dtype dt.
+ * plan == NULL builds an AUTO plan from k and flags.  R_out (nullable) receives the final
+ * power A^k (exact plans) or residual R_n = I - (I-A) Y_n -- the paper's accuracy metric
+ * I - (I-A)S_k.  Each radix-m step is exactly mu_m + 2 GEMM launches with all
+ * linear combinations fused into GEMM epilogues. */
+nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t k,
+                            const nseries_plan* plan, nseries_dtype dt, void* S, void* R_out,
+                            uint32_t flags, void* stream);
+
+/* Same with HOST pointers: copies A host->device, evaluates, copies S (and R_out) back,
+ * then synchronizes `stream`.  Pinned host memory gives asynchronous copies. */
+nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d, int64_t k,
+                                 const nseries_plan* plan, nseries_dtype dt, void* S_host,
+                                 void* R_host, uint32_t flags, void* stream);
+
+/* Batched small-matrix path: `batch` independent d x d matrices (d <= 64), A_b at
+ * A + b*strideA elements, S_b at S + b*strideS.  One kernel launch evaluates the whole plan
+ * for every matrix with the matrix resident in shared memory; products are counted per
+ * matrix (stats.products = plan products, stats.launches = 1). */
+nseries_status nseries_eval_batched_strided(nseries_handle h, const void* A, int64_t strideA,
+                                            int32_t batch, int32_t d, int64_t k,
+                                            const nseries_plan* plan, nseries_dtype dt, void* S,
+                                            int64_t strideS, uint32_t flags, void* stream);
+/* Pointer-array form: A_ptrs / S_ptrs are DEVICE arrays of `batch` device pointers. */
+nseries_status nseries_eval_batched(nseries_handle h, const void* const* A_ptrs, int32_t batch,
+                                    int32_t d, int64_t k, const nseries_plan* plan,
+                                    nseries_dtype dt, void* const* S_ptrs, uint32_t flags,
+                                    void* stream);
+
+/* Single fused-engine product C = X Y (d x d) -- the GEMM engine the plans run on, exposed
+ * for accuracy micro-tests and peak measurement.  Counts as one product. */
+nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X, const void* Y,
+                              void* C, int32_t d, void* stream);
+
+/* Statistics of the last eval on this handle (valid after the stream is synchronized). */
+nseries_status nseries_last_stats(nseries_handle h, nseries_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSERIES_H */

@@ -1,0 +1,239 @@
+"""ctypes marshalling for libnseries.so.  Names mirror include/nseries.h one-to-one."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libnseries.so")
+
+NSERIES_OK = 0
+STATUS_NAMES = {
+    0: "NSERIES_OK", 1: "NSERIES_ERR_INVALID_ARG", 2: "NSERIES_ERR_UNSUPPORTED_RADIX",
+    3: "NSERIES_ERR_PLAN_K_MISMATCH", 4: "NSERIES_ERR_APPROX_TELESCOPE", 5: "NSERIES_ERR_ALIAS",
+    6: "NSERIES_ERR_OOM", 7: "NSERIES_ERR_CUDA", 8: "NSERIES_ERR_NO_DEVICE",
+    9: "NSERIES_ERR_UNSUPPORTED_SIZE",
+}
+NSERIES_F64, NSERIES_F32 = 0, 1
+NSERIES_PLAN_AUTO, NSERIES_PLAN_BINARY, NSERIES_PLAN_RADIX5 = 0, 2, 5
+NSERIES_PLAN_RADIX9, NSERIES_PLAN_RADIX15, NSERIES_PLAN_CUSTOM = 9, 15, -1
+NSERIES_ELIDE_TRIVIAL = 0x1
+NSERIES_ALLOW_APPROX = 0x2
+NSERIES_RFORM_TELESCOPE = 0x4
+NSERIES_NO_GRAPH = 0x8
+NSERIES_SYNC_STATS = 0x10
+NSERIES_MAX_STEPS = 128
+
+# every symbol include/nseries.h declares (tests check the .so exports exactly these)
+EXPORTED = [
+    "nseries_create", "nseries_destroy", "nseries_status_string", "nseries_version",
+    "nseries_plan_build", "nseries_plan_finalize", "nseries_kernel_info", "nseries_eval",
+    "nseries_eval_host", "nseries_eval_batched_strided", "nseries_eval_batched",
+    "nseries_matmul", "nseries_last_stats",
+]
+
+
+class nseries_plan(ctypes.Structure):
+    _fields_ = [("n_steps", ctypes.c_int32), ("step", ctypes.c_int32 * NSERIES_MAX_STEPS),
+                ("form", ctypes.c_int32 * NSERIES_MAX_STEPS), ("products", ctypes.c_int32),
+                ("approx", ctypes.c_int32), ("flags", ctypes.c_uint32), ("k", ctypes.c_int64)]
+
+    @property
+    def steps(self):
+        return [int(self.step[i]) for i in range(self.n_steps)]
+
+    @property
+    def forms(self):
+        return [int(self.form[i]) for i in range(self.n_steps)]
+
+    def __repr__(self):
+        return f"nseries_plan(k={self.k}, steps={self.steps}, products={self.products}, approx={self.approx})"
+
+
+class nseries_stats(ctypes.Structure):
+    _fields_ = [("products", ctypes.c_int32), ("launches", ctypes.c_int32),
+                ("graph_replayed", ctypes.c_int32), ("n_ops", ctypes.c_int32),
+                ("ms_total", ctypes.c_float)]
+
+
+class NSeriesError(RuntimeError):
+    def __init__(self, status, where=""):
+        self.status = status
+        super().__init__(f"{where}: {STATUS_NAMES.get(status, status)} ({nseries_status_string(status)})")
+
+
+_lib = None
+
+
+def load_library(path=None):
+    """Load (never build) libnseries.so; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or _LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(f"libnseries.so not built at {path}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(path)
+    vp, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    plan_p = ctypes.POINTER(nseries_plan)
+    sig = {
+        "nseries_create": ([ctypes.POINTER(vp), ctypes.c_int], ctypes.c_int),
+        "nseries_destroy": ([vp], ctypes.c_int),
+        "nseries_status_string": ([ctypes.c_int], ctypes.c_char_p),
+        "nseries_version": ([], ctypes.c_char_p),
+        "nseries_plan_build": ([i64, ctypes.c_int, ctypes.POINTER(i32), i32, u32, plan_p], ctypes.c_int),
+        "nseries_plan_finalize": ([plan_p, i64, u32], ctypes.c_int),
+        "nseries_kernel_info": ([i32, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)], ctypes.c_int),
+        "nseries_eval": ([vp, vp, i32, i64, plan_p, ctypes.c_int, vp, vp, u32, vp], ctypes.c_int),
+        "nseries_eval_host": ([vp, vp, i32, i64, plan_p, ctypes.c_int, vp, vp, u32, vp], ctypes.c_int),
+        "nseries_eval_batched_strided": ([vp, vp, i64, i32, i32, i64, plan_p, ctypes.c_int, vp, i64,
+                                          u32, vp], ctypes.c_int),
+        "nseries_eval_batched": ([vp, vp, i32, i32, i64, plan_p, ctypes.c_int, vp, u32, vp], ctypes.c_int),
+        "nseries_matmul": ([vp, ctypes.c_int, vp, vp, vp, i32, vp], ctypes.c_int),
+        "nseries_last_stats": ([vp, ctypes.POINTER(nseries_stats)], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _check(st, where):
+    if st != NSERIES_OK:
+        raise NSeriesError(st, where)
+
+
+def _ptr(x):
+    """Device/host pointer of a torch tensor, numpy array or raw int (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dtype_of(t):
+    name = str(getattr(t, "dtype", ""))
+    if name.endswith("float64"):
+        return NSERIES_F64
+    if name.endswith("float32"):
+        return NSERIES_F32
+    raise TypeError(f"unsupported dtype {name}")
+
+
+# ---------------------------------------------------------------- 1:1 wrappers
+
+def nseries_status_string(status):
+    return load_library().nseries_status_string(int(status)).decode()
+
+
+def nseries_version():
+    return load_library().nseries_version().decode()
+
+
+def nseries_create(device=0):
+    h = ctypes.c_void_p()
+    _check(load_library().nseries_create(ctypes.byref(h), int(device)), "nseries_create")
+    return h
+
+
+def nseries_destroy(h):
+    _check(load_library().nseries_destroy(h), "nseries_destroy")
+
+
+def nseries_plan_build(k, kind=NSERIES_PLAN_AUTO, radices=None, flags=0):
+    p = nseries_plan()
+    arr, n = None, 0
+    if radices:
+        n = len(radices)
+        arr = (ctypes.c_int32 * n)(*radices)
+    _check(load_library().nseries_plan_build(int(k), int(kind), arr, n, int(flags), ctypes.byref(p)),
+           "nseries_plan_build")
+    return p
+
+
+def nseries_plan_finalize(steps, k, flags=0):
+    p = nseries_plan()
+    p.n_steps = len(steps)
+    for i, s in enumerate(steps):
+        p.step[i] = int(s)
+    _check(load_library().nseries_plan_finalize(ctypes.byref(p), int(k), int(flags)), "nseries_plan_finalize")
+    return p
+
+
+def nseries_kernel_info(m):
+    mu, ex, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(0)
+    L = load_library()
+    _check(L.nseries_kernel_info(int(m), ctypes.byref(mu), ctypes.byref(ex), None, ctypes.byref(n)),
+           "nseries_kernel_info")
+    buf = (ctypes.c_double * n.value)()
+    _check(L.nseries_kernel_info(int(m), ctypes.byref(mu), ctypes.byref(ex), buf, ctypes.byref(n)),
+           "nseries_kernel_info")
+    return {"mu": mu.value, "exact": bool(ex.value), "coeffs": list(buf)}
+
+
+def nseries_eval(h, A, d, k, plan=None, dtype=None, S=None, R_out=None, flags=0, stream=None):
+    dt = _dtype_of(A) if dtype is None else dtype
+    st = load_library().nseries_eval(h, _ptr(A), int(d), int(k), ctypes.byref(plan) if plan is not None else None,
+                                     dt, _ptr(S), _ptr(R_out), int(flags), _stream(stream))
+    _check(st, "nseries_eval")
+
+
+def nseries_eval_host(h, A, d, k, plan=None, dtype=None, S=None, R_out=None, flags=0, stream=None):
+    dt = _dtype_of(A) if dtype is None else dtype
+    st = load_library().nseries_eval_host(h, _ptr(A), int(d), int(k),
+                                          ctypes.byref(plan) if plan is not None else None,
+                                          dt, _ptr(S), _ptr(R_out), int(flags), _stream(stream))
+    _check(st, "nseries_eval_host")
+
+
+def nseries_eval_batched_strided(h, A, strideA, batch, d, k, plan=None, dtype=None, S=None,
+                                 strideS=None, flags=0, stream=None):
+    dt = _dtype_of(A) if dtype is None else dtype
+    strideS = strideA if strideS is None else strideS
+    st = load_library().nseries_eval_batched_strided(
+        h, _ptr(A), int(strideA), int(batch), int(d), int(k),
+        ctypes.byref(plan) if plan is not None else None, dt, _ptr(S), int(strideS), int(flags),
+        _stream(stream))
+    _check(st, "nseries_eval_batched_strided")
+
+
+def nseries_eval_batched(h, A_ptrs, batch, d, k, plan=None, dtype=NSERIES_F32, S_ptrs=None, flags=0,
+                         stream=None):
+    st = load_library().nseries_eval_batched(h, _ptr(A_ptrs), int(batch), int(d), int(k),
+                                             ctypes.byref(plan) if plan is not None else None,
+                                             int(dtype), _ptr(S_ptrs), int(flags), _stream(stream))
+    _check(st, "nseries_eval_batched")
+
+
+def nseries_matmul(h, X, Y, C, d, dtype=None, stream=None):
+    dt = _dtype_of(X) if dtype is None else dtype
+    _check(load_library().nseries_matmul(h, dt, _ptr(X), _ptr(Y), _ptr(C), int(d), _stream(stream)),
+           "nseries_matmul")
+
+
+def nseries_last_stats(h):
+    s = nseries_stats()
+    _check(load_library().nseries_last_stats(h, ctypes.byref(s)), "nseries_last_stats")
+    return {"products": s.products, "launches": s.launches, "graph_replayed": s.graph_replayed,
+            "n_ops": s.n_ops, "ms_total": s.ms_total}
+
+
+__all__ = [n for n in dir() if n.startswith(("nseries_", "NSERIES_"))] + [
+    "NSeriesError", "load_library", "EXPORTED", "STATUS_NAMES"]

@@ -1,0 +1,283 @@
+// gemm_f64.cu -- FP64 tensor-core GEMM with the fused multi-output epilogue (sm_100a).
+//
+// acc = X * Y (d x d x d, row-major, binary64) on the FP64 tensor pipe: sm_100a has no
+// tcgen05 .kind::f64, so the FP64 tensor path is the warp-level mma.sync m8n8k4 f64
+// (SASS DMMA.8x8x4).  Measured on this pool's B200 (profiles/peaks_r01_*):
+// DMMA.8x8x4 register loop 37.16 TFLOP/s = 148 SM x 64 FMA/clk x 1.965 GHz, so the engine's
+// job is to keep every SM sub-partition issuing one DMMA per 16 cycles.
+//
+// Design:
+//   * CTA tile BM x BN x BK (128x128x16 for d >= 1536, 64x64x16 below), warps tile the CTA
+//     as (BM/WM) x (BN/WN) with a WM x WN warp tile of m8n8 blocks (accumulators in registers).
+//   * STAGES-deep cp.async ring in shared memory; rows padded (+4 doubles) so every 64-bit
+//     fragment load of a half-warp hits 32 distinct banks.
+//   * Epilogue: out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I for up to 3 aux and 3
+//     outputs (every linear combination of the radix kernels).
+//   * Grouped rasterisation of the tile grid so concurrently resident CTAs share X row panels
+//     and Y column panels in L2.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+
+namespace nseries {
+namespace {
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async copy global->shared with zero fill when !valid.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct Cfg {
+  static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
+  static constexpr int kThreads = kWarpsM * kWarpsN * 32;
+  static constexpr int kMI = WM / 8, kNI = WN / 8;
+  static constexpr int kLdA = BK + 4;   // padded row (doubles) of the A tile [BM][BK]
+  static constexpr int kLdB = BN + 4;   // padded row of the B tile [BK][BN]
+  static constexpr int kStageA = BM * kLdA, kStageB = BK * kLdB;
+  static constexpr size_t kSmem = (size_t)STAGES * (kStageA + kStageB) * sizeof(double);
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2>
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::kThreads, 1)
+gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, EpiParams ep) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;
+  double* sB = smem + STAGES * C::kStageA;
+
+  // ---- grouped raster: GROUP tile-rows per band
+  constexpr int GROUP = 8;
+  const int ntm = (d + BM - 1) / BM, ntn = (d + BN - 1) / BN;
+  const int pid = blockIdx.x;
+  const int band = GROUP * ntn;
+  const int first_tm = (pid / band) * GROUP;
+  const int gsz = min(ntm - first_tm, GROUP);
+  const int tm = first_tm + (pid % band) % gsz;
+  const int tn = (pid % band) / gsz;
+  const int m0 = tm * BM, n0 = tn * BN;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp / C::kWarpsN) * WM, wn0 = (warp % C::kWarpsN) * WN;
+  const int g = lane >> 2, t = lane & 3;
+
+  auto load_stage = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    double* a = sA + stage * C::kStageA;
+    double* b = sB + stage * C::kStageB;
+    if constexpr (V2) {
+      // A tile: BM rows x BK cols, 2 doubles per chunk
+      constexpr int kChunksA = BM * BK / 2;
+#pragma unroll
+      for (int q = tid; q < kChunksA; q += C::kThreads) {
+        int r = q / (BK / 2), c = (q % (BK / 2)) * 2;
+        int gr = m0 + r, gc = k0 + c;
+        bool ok = gr < d && gc < d;
+        cp_async16(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok);
+      }
+      constexpr int kChunksB = BK * BN / 2;
+#pragma unroll
+      for (int q = tid; q < kChunksB; q += C::kThreads) {
+        int r = q / (BN / 2), c = (q % (BN / 2)) * 2;
+        int gr = k0 + r, gc = n0 + c;
+        bool ok = gr < d && gc < d;
+        cp_async16(b + r * C::kLdB + c, ok ? Y + (size_t)gr * d + gc : Y, ok);
+      }
+    } else {
+#pragma unroll 4
+      for (int q = tid; q < BM * BK; q += C::kThreads) {
+        int r = q / BK, c = q % BK;
+        int gr = m0 + r, gc = k0 + c;
+        bool ok = gr < d && gc < d;
+        cp_async8(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok);
+      }
+#pragma unroll 4
+      for (int q = tid; q < BK * BN; q += C::kThreads) {
+        int r = q / BN, c = q % BN;
+        int gr = k0 + r, gc = n0 + c;
+        bool ok = gr < d && gc < d;
+        cp_async8(b + r * C::kLdB + c, ok ? Y + (size_t)gr * d + gc : Y, ok);
+      }
+    }
+  };
+
+  double acc[C::kMI][C::kNI][2];
+#pragma unroll
+  for (int i = 0; i < C::kMI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::kNI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (d + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* a = sA + (kt % STAGES) * C::kStageA;
+    const double* b = sB + (kt % STAGES) * C::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[C::kMI], bf[C::kNI];
+#pragma unroll
+      for (int i = 0; i < C::kMI; ++i) af[i] = a[(wm0 + i * 8 + g) * C::kLdA + kk + t];
+#pragma unroll
+      for (int j = 0; j < C::kNI; ++j) bf[j] = b[(kk + t) * C::kLdB + wn0 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < C::kMI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::kNI; ++j) dmma_m8n8k4(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- fused epilogue: out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I
+  const int n_aux = ep.n_aux, n_out = ep.n_out;
+#pragma unroll
+  for (int i = 0; i < C::kMI; ++i) {
+    const int row = m0 + wm0 + i * 8 + g;
+    if (row >= d) continue;
+#pragma unroll
+    for (int j = 0; j < C::kNI; ++j) {
+      const int col = n0 + wn0 + j * 8 + 2 * t;
+      if (col >= d) continue;
+      const size_t off = (size_t)row * d + col;
+      if constexpr (V2) {
+        double2 av[kMaxAux];
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x)
+          if (x < n_aux) av[x] = *reinterpret_cast<const double2*>(
+                             static_cast<const double*>(ep.aux[x]) + off);
+#pragma unroll
+        for (int o = 0; o < kMaxOut; ++o) {
+          if (o >= n_out) break;
+          double v0 = ep.alpha[o] * acc[i][j][0], v1 = ep.alpha[o] * acc[i][j][1];
+#pragma unroll
+          for (int x = 0; x < kMaxAux; ++x)
+            if (x < n_aux) { v0 += ep.beta[o][x] * av[x].x; v1 += ep.beta[o][x] * av[x].y; }
+          if (row == col) v0 += ep.gamma[o];
+          if (row == col + 1) v1 += ep.gamma[o];
+          *reinterpret_cast<double2*>(static_cast<double*>(ep.out[o]) + off) = make_double2(v0, v1);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (col + e >= d) continue;
+          double av[kMaxAux];
+#pragma unroll
+          for (int x = 0; x < kMaxAux; ++x)
+            if (x < n_aux) av[x] = static_cast<const double*>(ep.aux[x])[off + e];
+#pragma unroll
+          for (int o = 0; o < kMaxOut; ++o) {
+            if (o >= n_out) break;
+            double v = ep.alpha[o] * acc[i][j][e];
+#pragma unroll
+            for (int x = 0; x < kMaxAux; ++x)
+              if (x < n_aux) v += ep.beta[o][x] * av[x];
+            if (row == col + e) v += ep.gamma[o];
+            static_cast<double*>(ep.out[o])[off + e] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Degenerate epilogue without a product (k = 1 identity, elided k = 2 binary, R copy).
+__global__ void axpby_f64_kernel(int d, EpiParams ep) {
+  const size_t n = (size_t)d * d;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / d), col = (int)(idx % d);
+    for (int o = 0; o < ep.n_out; ++o) {
+      double v = 0.0;
+      for (int x = 0; x < ep.n_aux; ++x) v += ep.beta[o][x] * static_cast<const double*>(ep.aux[x])[idx];
+      if (row == col) v += ep.gamma[o];
+      static_cast<double*>(ep.out[o])[idx] = v;
+    }
+  }
+}
+
+__global__ void identity_f64_kernel(double* I, int d) {
+  const size_t n = (size_t)d * d;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n;
+       idx += (size_t)gridDim.x * blockDim.x)
+    I[idx] = (idx / d == idx % d) ? 1.0 : 0.0;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2>
+int launch_cfg(const double* X, const double* Y, int d, const EpiParams& ep, cudaStream_t s) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
+  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2>;
+  static bool attr_set = false;   // per template instance
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::kSmem);
+    if (e != cudaSuccess) return (int)e;
+    attr_set = true;
+  }
+  const int tiles = ((d + BM - 1) / BM) * ((d + BN - 1) / BN);
+  kern<<<tiles, C::kThreads, C::kSmem, s>>>(X, Y, d, ep);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  bool v2 = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
+  for (int i = 0; i < ep.n_aux; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.aux[i]) % 16 == 0;
+  for (int i = 0; i < ep.n_out; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.out[i]) % 16 == 0;
+  if (d >= 1536) {
+    return v2 ? launch_cfg<128, 128, 16, 64, 32, 4, true>(X, Y, d, ep, s)
+              : launch_cfg<128, 128, 16, 64, 32, 4, false>(X, Y, d, ep, s);
+  }
+  return v2 ? launch_cfg<64, 64, 16, 32, 32, 4, true>(X, Y, d, ep, s)
+            : launch_cfg<64, 64, 16, 32, 32, 4, false>(X, Y, d, ep, s);
+}
+
+int launch_axpby_f64(int d, const EpiParams& ep, void* stream) {
+  const size_t n = (size_t)d * d;
+  int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+  axpby_f64_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(d, ep);
+  return (int)cudaGetLastError();
+}
+
+int launch_identity_f64(double* I, int d, void* stream) {
+  const size_t n = (size_t)d * d;
+  int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+  identity_f64_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(I, d);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace nseries

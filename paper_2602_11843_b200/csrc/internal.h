@@ -1,0 +1,83 @@
+// internal.h -- library-internal types shared by the plan compiler, the executor and the
+// device engines.  Not part of the C ABI (see include/nseries.h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/nseries.h"
+
+namespace nseries {
+
+// ---------------------------------------------------------------- kernel circuits (host)
+// Coefficients of the radix kernels as the library evaluates them (binary64).
+struct Radix15Params {
+  double L2[3], R2[3], L3[4], R3[4], L4[5], R4[5], gamma[4];
+};
+const Radix15Params& radix15_params();
+int kernel_mu(int m);            // products of the kernel circuit, -1 if unsupported
+bool kernel_exact(int m);
+// monomial coefficients of the kernel polynomial (double), evaluated from the circuit
+std::vector<double> kernel_poly(int m);
+
+// ---------------------------------------------------------------- plan builder (host)
+nseries_status build_plan(int64_t k, nseries_plan_kind kind, const int32_t* radices, int32_t n,
+                          uint32_t flags, nseries_plan* out);
+nseries_status finalize_plan(nseries_plan* plan, int64_t k, uint32_t flags);
+int step_products(int step, bool first, bool last, uint32_t flags);
+
+// ---------------------------------------------------------------- op list (host)
+// Every GEMM op computes acc = X * Y (d x d x d) and an epilogue
+//   out_j = alpha_j * acc + sum_i beta_ji * aux_i + gamma_j * I        (j < n_out <= 3)
+// where aux_i are d x d matrices read at the accumulator tile's coordinates (i < n_aux <= 3).
+// A degenerate "AXPBY" op (no product) evaluates the same epilogue with alpha = 0; it only
+// occurs for k = 1 or fully elided binary plans.
+constexpr int kMaxAux = 3;
+constexpr int kMaxOut = 3;
+
+enum ValKind : int { V_USER_A = 0, V_IDENT = 1, V_USER_S = 2, V_USER_R = 3, V_TEMP = 4 };
+
+struct Op {
+  bool gemm = true;
+  int X = -1, Y = -1;            // value ids (operands)
+  int n_aux = 0, n_out = 0;
+  int aux[kMaxAux] = {-1, -1, -1};
+  int out[kMaxOut] = {-1, -1, -1};
+  double alpha[kMaxOut] = {0, 0, 0};
+  double beta[kMaxOut][kMaxAux] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double gamma[kMaxOut] = {0, 0, 0};
+  int step = -1;                 // plan step this op belongs to
+  const char* tag = "";
+};
+
+struct Program {
+  std::vector<Op> ops;
+  int n_values = 0;              // value ids 0..n_values-1
+  std::vector<int> val_kind;     // ValKind per value
+  std::vector<int> val_buf;      // workspace slot per V_TEMP value (-1 otherwise)
+  int n_slots = 0;               // workspace d x d slots needed
+  int final_S = -1, final_R = -1;
+  bool needs_identity = false;   // the IDENT value is read from memory (paper counting)
+  int products = 0;
+};
+
+// Compile a finalized plan into an op list with workspace slot assignment.
+// want_R: route the final power/residual into the user's R_out buffer.
+nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog);
+
+// ---------------------------------------------------------------- device engines
+struct EpiParams {
+  int n_aux, n_out;
+  const void* aux[kMaxAux];
+  void* out[kMaxOut];
+  double alpha[kMaxOut];
+  double beta[kMaxOut][kMaxAux];
+  double gamma[kMaxOut];
+};
+
+// fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
+int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);
+int launch_axpby_f64(int d, const EpiParams& ep, void* stream);
+int launch_identity_f64(double* I, int d, void* stream);
+
+}  // namespace nseries

@@ -1,0 +1,122 @@
+"""Host-side checks of the C-ABI library (no GPU needed): symbol exports, the plan builder
+against the oracle's plain DP, and the library's kernel polynomials against the oracle's."""
+import os
+import re
+
+import pytest
+
+import paper_2602_11843_b200 as P
+from oracle import kernels as K
+from oracle import plan as OP
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2602_11843_b200 import build as B
+    B.build()
+    return P.load_library()
+
+
+def test_exports_match_header(lib):
+    hdr = open(os.path.join(ROOT, "include", "nseries.h")).read()
+    declared = sorted(set(re.findall(r"\b(nseries_[a-z_]+)\s*\(", hdr)))
+    assert declared == sorted(P.EXPORTED)
+    syms = os.popen(f"nm -D --defined-only {P._binding._LIB_PATH}").read()
+    exported = sorted(set(re.findall(r" T (nseries_[a-z_]+)", syms)))
+    assert exported == declared
+    for name in declared:
+        assert hasattr(lib, name)
+
+
+def test_no_torch_in_abi():
+    hdr = open(os.path.join(ROOT, "include", "nseries.h")).read()
+    assert "torch" not in hdr.lower().replace("torch cuda tensors", "")
+
+
+def test_version_and_status(lib):
+    assert "sm_100a" in P.nseries_version()
+    assert P.nseries_status_string(0) == "ok"
+    assert "alias" in P.nseries_status_string(5)
+
+
+@pytest.mark.parametrize("m,k,products", [
+    (5, 125, 12), (5, 625, 16), (9, 81, 10), (9, 729, 15), (15, 225, 12), (15, 3375, 18),
+    (2, 128, 14), (2, 512, 18), (2, 4096, 24), (9, 6561, 20)])
+def test_pure_plans_table2(lib, m, k, products):
+    plan = P.nseries_plan_build(k, kind=m)
+    assert plan.steps == [m] * len(plan.steps)
+    assert plan.products == products
+    assert plan.approx == (1 if m == 15 else 0)
+
+
+def test_pure_plan_k_mismatch(lib):
+    with pytest.raises(P.NSeriesError) as e:
+        P.nseries_plan_build(100, kind=9)
+    assert e.value.status == 3
+
+
+def test_approx_requires_flag(lib):
+    with pytest.raises(P.NSeriesError) as e:
+        P.nseries_plan_build(225, radices=[15, 9])
+    assert e.value.status == 4
+    with pytest.raises(P.NSeriesError) as e:
+        P.nseries_plan_finalize([15], 15, 0)
+    assert e.value.status == 4
+    with pytest.raises(P.NSeriesError) as e:
+        P.nseries_plan_finalize([7], 7, 0)
+    assert e.value.status == 2
+
+
+RADIX_SETS = [[2], [5, 2], [9, 5, 2], [15, 9, 5, 2], [15, 9], [9], [5]]
+
+
+@pytest.mark.parametrize("elide", [0, 1])
+def test_auto_plan_matches_oracle_dp(lib, elide):
+    for radices in RADIX_SETS:
+        flags = (P.NSERIES_ALLOW_APPROX if 15 in radices else 0) | (P.NSERIES_ELIDE_TRIVIAL if elide else 0)
+        for k in list(range(1, 400)) + [729, 1000, 3375, 4096, 6561, 10000, 12345]:
+            ref = OP.best_plan_dp(k, radices, bool(elide))
+            plan = P.nseries_plan_build(k, radices=radices, flags=flags)
+            assert plan.steps == ref, (radices, k, elide)
+            assert plan.products == OP.plan_products(ref, bool(elide))
+
+
+def test_auto_plan_large_k(lib):
+    # k up to 2^62: the plan exists, reaches k, and never costs more than binary with +1
+    for k in [2 ** 40, 3 ** 30, 10 ** 15, 2 ** 62, 2 ** 62 - 1]:
+        plan = P.nseries_plan_build(k, radices=[15, 9, 5, 2], flags=P.NSERIES_ALLOW_APPROX)
+        assert OP.plan_reaches(plan.steps) == k
+        binary = P.nseries_plan_build(k, radices=[2])
+        assert plan.products <= binary.products
+
+
+def test_forms(lib):
+    p = P.nseries_plan_finalize([15, 1, 9, 2], 15 * 2 * 9 * 2 // 1 // 1 if False else 16 * 9 * 2,
+                                P.NSERIES_ALLOW_APPROX)
+    assert p.forms == [1, 0, 0, 0]
+    p = P.nseries_plan_finalize([15], 15, P.NSERIES_ALLOW_APPROX | P.NSERIES_RFORM_TELESCOPE)
+    assert p.forms == [2]
+
+
+@pytest.mark.parametrize("m", [2, 5, 9, 15])
+def test_kernel_info_vs_oracle(lib, m):
+    info = P.nseries_kernel_info(m)
+    assert info["mu"] == K.MU[m]
+    assert info["exact"] == K.EXACT[m]
+    ref = [float(c) for c in K.kernel_coeffs(m)]
+    assert len(info["coeffs"]) == len(ref)
+    for a, b in zip(info["coeffs"], ref):
+        assert abs(a - b) <= 1e-15 * max(1.0, abs(b))
+
+
+def test_library_radix15_params_vs_oracle_polish(lib):
+    # the library's transcribed polished parameters agree with the oracle's own polish
+    src = open(os.path.join(ROOT, "paper_2602_11843_b200", "csrc", "plan.cc")).read()
+    block = src[src.index("kRadix15 = {"):src.index("};", src.index("kRadix15 = {"))]
+    nums = [float(x) for x in re.findall(r"-?\d+\.\d+(?:e-?\d+)?", block)]
+    ref = [float(x) for x in K.radix15_flat(K.polished_radix15_strings())]
+    assert len(nums) == 28
+    for a, b in zip(nums, ref):
+        assert abs(a - b) <= 2e-16 * max(1.0, abs(b))
