@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""bench.py -- S_k(A) evals/s and TFLOP/s at d=4096 (BASELINE.json metric, configs[2]).
+
+One step = one evaluation of S_k(A) through the C ABI (nseries_eval) on the headline plan:
+config 3 (d=4096, fp64, spectrum [0, 0.995]), radix-15 x3 in the residual framework
+(k=3375, 18 products in the paper's counting).  The same run also times the radix-9 x4
+(k=6561) and binary x12 (k=4096) plans ("per_plan") for the wall-time ratio targets.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+N > 1 (under torchrun): the single-matrix path does not shard (DESIGN.md "Multi-GPU:
+replicas only"); each rank evaluates its own replica, value = all ranks' evals / max time.
+--impl reference times the oracle (oracle/, long double, host cores) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "S_k(A) evals/sec and TFLOP/s (% of FP64/TF32 tensor peak) at d=4096, per radix plan"
+D = 4096
+HEADLINE = ([15, 15, 15], 3375)
+PLANS = {"x15^3": ([15, 15, 15], 3375), "x9^4": ([9, 9, 9, 9], 6561), "x2^12": ([2] * 12, 4096)}
+# Roofline denominator for the FP64 tensor pipe: measured DMMA.8x8x4 register-loop peak on
+# this pool's B200 (tools/peak_fp64.cu -> profiles/peaks_r01_fp64_microbench.json).
+FP64_PEAK_TFLOPS = 37.161
+FP64_PEAK_SOURCE = "measured: DMMA m8n8k4 register loop, tools/peak_fp64.cu (profiles/peaks_r01_fp64_microbench.json)"
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-plan", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 2 + len(REASONS):
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        reasons = sorted({REASONS[i] for r in self.rows for i in range(len(REASONS))
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup(n):
+    if n <= 1 or "RANK" not in os.environ:
+        return 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    return dist.get_rank(), dist.get_world_size(), local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ oracle (CPU) legs
+
+def oracle_sample(A_np, steps, n_cols=1):
+    """Time the oracle (as it stands) on n_cols probe columns of the workload; returns
+    (seconds per column, threads)."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2602_11843_b200 import inputs
+    V, _ = inputs.probe_block(A_np.shape[0], 2, n_unit=n_cols, n_gauss=0)
+    t0 = time.perf_counter()
+    if 15 in steps:
+        O.plan_apply(A_np, steps, V)
+    else:
+        k = 1
+        for s in steps:
+            k = k + 1 if s == 1 else k * s
+        O.series_sum(A_np, k, V)
+    return (time.perf_counter() - t0) / n_cols, O.num_threads()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    from paper_2602_11843_b200 import inputs
+    A_np = inputs.cfg3(D, device="cpu")[0] if not _cuda_ok() else inputs.cfg3(D, device="cuda")[0].cpu().numpy()
+    steps, k = HEADLINE
+    for _ in range(args.warmup):
+        oracle_sample(A_np, steps)
+    times = []
+    threads = 1
+    for _ in range(args.steps):
+        t, threads = oracle_sample(A_np, steps)
+        times.append(t)
+    per_col = sum(times) / len(times)
+    per_eval = per_col * D
+    value = 1.0 / per_eval
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_col * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f80 (x87 long double)",
+        "data": "synthetic",
+        "config": {"workload": "cfg3 d=4096 spectrum[0,0.995] radix-15x3 k=3375", "d": D, "k": k, "plan": "x15^3"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "oracle",
+                         "sample": "per step: oracle C-2 (compositional Horner, 4912 long-double matvecs) on 1 of "
+                                   "4096 columns; evals/s = 1/(seconds per column x 4096)"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cuda_ok():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+# ------------------------------------------------------------------ native leg
+
+def time_plan(P, h, A, S, steps, k, n_steps, n_warm, flags, stream, world):
+    import torch
+    plan = P.nseries_plan_finalize(steps, k, flags)
+    for _ in range(n_warm):
+        P.nseries_eval(h, A, D, k, plan=plan, S=S, flags=flags, stream=stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n_steps):
+        P.nseries_eval(h, A, D, k, plan=plan, S=S, flags=flags, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    st = P.nseries_last_stats(h)
+    return max_over_ranks(ms, world), plan, st
+
+
+def run_native(args):
+    import numpy as np
+    import torch
+    rank, world, local = dist_setup(args.gpus)
+    import paper_2602_11843_b200 as P
+    P.load_library()
+    from paper_2602_11843_b200 import inputs
+    torch.cuda.set_device(local)
+    h = P.nseries_create(local)
+    A, _, _ = inputs.cfg3(D, seed=2, device="cuda")
+    A = A.contiguous()
+    S = torch.empty_like(A)
+    stream = torch.cuda.current_stream()
+    steps, k = HEADLINE
+    flags = P.NSERIES_ALLOW_APPROX
+    flop_per_product = 2.0 * D ** 3
+
+    with ClockSampler(local) as clk:
+        ms, plan, st = time_plan(P, h, A, S, steps, k, args.steps, max(args.warmup, 3), flags, stream, world)
+    clocks = clk.summary()
+    ms_step = ms / args.steps
+    evals_per_s = world * args.steps / (ms / 1e3)
+    tflops = plan.products * flop_per_product / (ms_step * 1e-3) / 1e12
+
+    per_plan = {}
+    if not args.no_per_plan:
+        for name, (stp, kk) in PLANS.items():
+            fl = P.NSERIES_ALLOW_APPROX if 15 in stp else 0
+            n = max(2, args.steps // 2)
+            pms, pplan, _ = time_plan(P, h, A, S, stp, kk, n, 2, fl, stream, world)
+            pstep = pms / n
+            per_plan[name] = {"k": kk, "products": pplan.products, "ms_per_eval": pstep,
+                              "evals_per_s": world * 1e3 / pstep,
+                              "tflops": pplan.products * flop_per_product / (pstep * 1e-3) / 1e12}
+        b = per_plan["x2^12"]
+        for name in ("x15^3", "x9^4"):
+            p = per_plan[name]
+            p["time_ratio_vs_binary"] = p["ms_per_eval"] / b["ms_per_eval"]
+            p["target_ratio"] = (p["products"] / b["products"]) / 0.95
+
+    # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
+    A_host = A.cpu().pin_memory()
+    S_host = torch.empty_like(A_host).pin_memory()
+    plan = P.nseries_plan_finalize(steps, k, flags)
+    for _ in range(2):
+        P.nseries_eval_host(h, A_host, D, k, plan=plan, S=S_host, flags=flags, stream=stream)
+    barrier(world)
+    n_e2e = max(2, args.steps // 2)
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        P.nseries_eval_host(h, A_host, D, k, plan=plan, S=S_host, flags=flags, stream=stream)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    e2e_val = world * n_e2e / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        A_np = A.cpu().numpy()
+        per_col, threads = oracle_sample(A_np, steps)
+        cpu = {"value": 1.0 / (per_col * D), "unit": "evals/s", "cores": threads, "kind": "oracle",
+               "sample": f"oracle C-2 (compositional Horner, 4912 long-double matvecs) on 1 of {D} columns "
+                         f"({per_col:.1f} s); evals/s = 1/(s per column x {D})"}
+
+    roof = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": tflops / FP64_PEAK_TFLOPS, "traffic": _traffic(),
+            "kernel": "gemm_f64_kernel<128,128,16,64,32,4> (DMMA.8x8x4)",
+            "algorithmic_flops_per_launch": flop_per_product,
+            "note": "achieved = 2 d^3 per GEMM launch / average launch duration over the timed region "
+                    "(every launch in the step is this kernel); peak " + FP64_PEAK_SOURCE}
+    line = {
+        "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 d=4096 fp64, A = Q diag(1-lam) Q^T, lam~U[0.005,1] (seed 2); radix-15x3 residual plan k=3375",
+                   "d": D, "k": k, "plan": "x15^3", "products": plan.products,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (A 128 MiB + ~1 GiB workspace per eval > 126 MB L2)"},
+        "tflops": tflops, "products": plan.products,
+        "roofline": roof, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": D * D * 8,
+                "d2h_bytes_per_step": D * D * 8},
+        "gpu_launches": st["launches"] * args.steps,
+        "clocks": clocks,
+        "per_plan": per_plan,
+    }
+    P.nseries_destroy(h)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def _traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_gemm_f64_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
