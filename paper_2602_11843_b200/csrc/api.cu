@@ -289,22 +289,90 @@ nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d
   return cuda_fail(h, cudaStreamSynchronize(s));
 }
 
+static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t strideA,
+                                        const void* const* A_ptrs, int32_t batch, int32_t d,
+                                        int64_t k, const nseries_plan* plan, nseries_dtype dt,
+                                        void* S, int64_t strideS, void* const* S_ptrs,
+                                        uint32_t flags, void* stream) {
+  if (!h) return NSERIES_ERR_INVALID_ARG;
+  if (h->sticky != NSERIES_OK) return h->sticky;
+  if (batch < 0 || d < 1 || k < 1) return NSERIES_ERR_INVALID_ARG;
+  if (dt != NSERIES_F64 && dt != NSERIES_F32) return NSERIES_ERR_INVALID_ARG;
+  if ((dt == NSERIES_F32 && d > 64) || (dt == NSERIES_F64 && d > 32)) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  nseries_plan p;
+  nseries_status st = resolve_plan(plan, k, flags, &p);
+  if (st != NSERIES_OK) return st;
+  std::string key = plan_key(p, false);
+  auto it = h->programs.find(key);
+  if (it == h->programs.end()) {
+    Program prog;
+    st = compile_plan(p, false, &prog);
+    if (st != NSERIES_OK) return st;
+    it = h->programs.emplace(key, std::move(prog)).first;
+  }
+  const Program& P = it->second;
+  if ((int)P.ops.size() > kMaxBatchedOps) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  BatchedProgram bp{};
+  bp.n_ops = (int)P.ops.size();
+  bp.a_slot = P.n_slots;
+  bp.ident_slot = P.n_slots + 1;
+  bp.s_slot = P.n_slots + 2;
+  bp.n_slots = P.n_slots + 3;
+  auto slot = [&](int v) -> int {
+    switch (P.val_kind[v]) {
+      case V_USER_A: return bp.a_slot;
+      case V_IDENT: return bp.ident_slot;
+      case V_USER_S: return bp.s_slot;
+      case V_TEMP: return P.val_buf[v];
+      default: return -1;
+    }
+  };
+  for (int i = 0; i < bp.n_ops; ++i) {
+    const Op& op = P.ops[i];
+    BatchedOp& b = bp.ops[i];
+    b.gemm = op.gemm ? 1 : 0;
+    b.X = op.gemm ? (int8_t)slot(op.X) : 0;
+    b.Y = op.gemm ? (int8_t)slot(op.Y) : 0;
+    b.n_aux = (int8_t)op.n_aux;
+    b.n_out = (int8_t)op.n_out;
+    for (int a = 0; a < kMaxAux; ++a) b.aux[a] = a < op.n_aux ? (int8_t)slot(op.aux[a]) : 0;
+    for (int j = 0; j < kMaxOut; ++j) {
+      b.out[j] = j < op.n_out ? (int8_t)slot(op.out[j]) : 0;
+      b.alpha[j] = op.alpha[j];
+      b.gamma[j] = op.gamma[j];
+      for (int a = 0; a < kMaxAux; ++a) b.beta[j][a] = op.beta[j][a];
+    }
+  }
+  h->stats = nseries_stats{};
+  h->stats.products = P.products;
+  h->stats.n_ops = bp.n_ops;
+  if (batch == 0) return NSERIES_OK;
+  if ((!A && !A_ptrs) || (!S && !S_ptrs)) return NSERIES_ERR_INVALID_ARG;
+  if (A && A == S) return NSERIES_ERR_ALIAS;
+  cudaSetDevice(h->device);
+  int rc = launch_batched(dt, A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, bp, stream);
+  if (rc == -1) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+  h->stats.launches = 1;
+  return NSERIES_OK;
+}
+
 nseries_status nseries_eval_batched_strided(nseries_handle h, const void* A, int64_t strideA,
                                             int32_t batch, int32_t d, int64_t k,
                                             const nseries_plan* plan, nseries_dtype dt, void* S,
                                             int64_t strideS, uint32_t flags, void* stream) {
-  (void)h; (void)A; (void)strideA; (void)batch; (void)d; (void)k; (void)plan; (void)dt;
-  (void)S; (void)strideS; (void)flags; (void)stream;
-  return NSERIES_ERR_UNSUPPORTED_SIZE;
+  if (strideA < (int64_t)d * d || strideS < (int64_t)d * d) return NSERIES_ERR_INVALID_ARG;
+  return eval_batched_impl(h, A, strideA, nullptr, batch, d, k, plan, dt, S, strideS, nullptr,
+                           flags, stream);
 }
 
 nseries_status nseries_eval_batched(nseries_handle h, const void* const* A_ptrs, int32_t batch,
                                     int32_t d, int64_t k, const nseries_plan* plan,
                                     nseries_dtype dt, void* const* S_ptrs, uint32_t flags,
                                     void* stream) {
-  (void)h; (void)A_ptrs; (void)batch; (void)d; (void)k; (void)plan; (void)dt; (void)S_ptrs;
-  (void)flags; (void)stream;
-  return NSERIES_ERR_UNSUPPORTED_SIZE;
+  if (batch > 0 && (!A_ptrs || !S_ptrs)) return NSERIES_ERR_INVALID_ARG;
+  return eval_batched_impl(h, nullptr, 0, A_ptrs, batch, d, k, plan, dt, nullptr, 0, S_ptrs, flags,
+                           stream);
 }
 
 nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X, const void* Y,

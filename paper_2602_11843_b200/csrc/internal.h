@@ -75,6 +75,23 @@ struct EpiParams {
   double gamma[kMaxOut];
 };
 
+// Batched small-matrix path: the compiled op list with values mapped to shared-memory slots.
+constexpr int kMaxBatchedOps = 48;
+struct BatchedOp {
+  int8_t gemm, X, Y, n_aux, n_out, aux[kMaxAux], out[kMaxOut];
+  double alpha[kMaxOut];
+  double beta[kMaxOut][kMaxAux];
+  double gamma[kMaxOut];
+};
+struct BatchedProgram {
+  int n_ops, n_slots, a_slot, ident_slot, s_slot;
+  BatchedOp ops[kMaxBatchedOps];
+};
+// returns 0 on success, -1 if the size is unsupported, else a cudaError_t
+int launch_batched(nseries_dtype dt, const void* A, int64_t strideA, const void* const* A_ptrs,
+                   void* S, int64_t strideS, void* const* S_ptrs, int batch, int d,
+                   const BatchedProgram& prog, void* stream);
+
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);
 int launch_axpby_f64(int d, const EpiParams& ep, void* stream);
