@@ -66,14 +66,24 @@ nseries_status ensure_identity(nseries_ctx* h, int d, nseries_dtype dt, cudaStre
     cudaFree(h->ident);
     h->ident = nullptr;
   }
-  cudaError_t e = cudaMalloc(&h->ident, (size_t)d * d * elem_size(dt));
+  const size_t bytes = dt == NSERIES_F64 ? (size_t)d * d * sizeof(double)
+                                          : 2 * (size_t)d * padded_ld(d) * sizeof(float);
+  cudaError_t e = cudaMalloc(&h->ident, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return NSERIES_ERR_OOM;
   }
   h->ident_d = d;
   h->ident_dt = dt;
-  int rc = launch_identity_f64(static_cast<double*>(h->ident), d, s);
+  int rc;
+  if (dt == NSERIES_F64) {
+    rc = launch_identity_f64(static_cast<double*>(h->ident), d, s);
+  } else {
+    float* hi = static_cast<float*>(h->ident);
+    float* lo = hi + (size_t)d * padded_ld(d);
+    cudaMemsetAsync(h->ident, 0, bytes, s);
+    rc = launch_split_f32(nullptr, 0, hi, lo, nullptr, nullptr, padded_ld(d), d, true, s);
+  }
   return cuda_fail(h, (cudaError_t)rc);
 }
 
@@ -88,6 +98,111 @@ nseries_status resolve_plan(const nseries_plan* plan, int64_t k, uint32_t flags,
   *out = *plan;
   if (out->k != k) return NSERIES_ERR_PLAN_K_MISMATCH;
   return finalize_plan(out, k, plan->flags | (flags & (NSERIES_ALLOW_APPROX)));
+}
+
+// fp32: every value has up to five planes -- x (fp32 value: aux reads, returned S/R), hi/lo
+// (tf32 operand planes for the left GEMM role, row-major) and hiT/loT (right role,
+// transposed: the tcgen05 B operand must be K-major for .kind::tf32).  Planes are d x ldp.
+// Slot i < n_slots holds temp value i's planes; slots n_slots..+2 hold the operand planes of
+// the user's A, S and R buffers (their x planes are the user buffers, ld = d).
+constexpr int kF32Planes = 5;
+size_t f32_ws_bytes(const Program& P, int d) {
+  return (size_t)(P.n_slots + 3) * kF32Planes * d * padded_ld(d) * sizeof(float);
+}
+
+nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A, float* S, float* R,
+                               int d, cudaStream_t s, int* launches) {
+  const int ldp = padded_ld(d);
+  const size_t plane = (size_t)d * ldp;
+  float* ws = static_cast<float*>(h->ws);
+  // --- operand roles: X.Y = Y.X (all values are polynomials in A), so each GEMM may put
+  // either factor on the left; pick the order that needs the fewest new plane layouts.
+  std::vector<int> role(P.n_values, 0);          // bit 0: left (row planes), bit 1: right (T)
+  std::vector<std::pair<int, int>> lr(P.ops.size(), {-1, -1});
+  const int ident = 1;
+  role[ident] = 3;
+  for (size_t i = 0; i < P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    if (!op.gemm) continue;
+    auto cost = [&](int l, int r) { return ((role[l] & 1) ? 0 : 1) + ((role[r] & 2) ? 0 : 1); };
+    int l = op.X, r = op.Y;
+    if (cost(op.Y, op.X) < cost(op.X, op.Y)) std::swap(l, r);
+    role[l] |= 1;
+    role[r] |= 2;
+    lr[i] = {l, r};
+  }
+  auto slot_of = [&](int v) -> int {
+    switch (P.val_kind[v]) {
+      case V_USER_A: return P.n_slots;
+      case V_USER_S: return P.n_slots + 1;
+      case V_USER_R: return P.n_slots + 2;
+      case V_TEMP: return P.val_buf[v];
+      default: return -1;
+    }
+  };
+  auto planes = [&](int v) -> float* { return ws + (size_t)slot_of(v) * kF32Planes * plane; };
+  auto xplane = [&](int v, int* ld) -> float* {
+    switch (P.val_kind[v]) {
+      case V_USER_A: *ld = d; return const_cast<float*>(A);
+      case V_USER_S: *ld = d; return S;
+      case V_USER_R: *ld = d; return R;
+      case V_TEMP: *ld = ldp; return planes(v);
+      default: *ld = ldp; return nullptr;
+    }
+  };
+  float* id_hi = static_cast<float*>(h->ident);
+  float* id_lo = id_hi + plane;
+  auto hi = [&](int v) { return P.val_kind[v] == V_IDENT ? id_hi : planes(v) + plane; };
+  auto lo = [&](int v) { return P.val_kind[v] == V_IDENT ? id_lo : planes(v) + 2 * plane; };
+  auto hiT = [&](int v) { return P.val_kind[v] == V_IDENT ? id_hi : planes(v) + 3 * plane; };
+  auto loT = [&](int v) { return P.val_kind[v] == V_IDENT ? id_lo : planes(v) + 4 * plane; };
+  int nl = 0;
+  const int vA = 0;
+  if (role[vA]) {   // one-off split of the user's A into the engine's operand planes
+    int rc = launch_split_f32(A, d, (role[vA] & 1) ? hi(vA) : nullptr, (role[vA] & 1) ? lo(vA) : nullptr,
+                              (role[vA] & 2) ? hiT(vA) : nullptr, (role[vA] & 2) ? loT(vA) : nullptr,
+                              ldp, d, false, s);
+    if (rc) return cuda_fail(h, (cudaError_t)rc);
+    ++nl;
+  }
+  std::vector<char> needx(P.n_values, 0);
+  for (const Op& op : P.ops)
+    for (int i = 0; i < op.n_aux; ++i) needx[op.aux[i]] = 1;
+  if (P.final_S >= 0) needx[P.final_S] = 1;
+  if (P.final_R >= 0) needx[P.final_R] = 1;
+  for (size_t i = 0; i < P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    EpiParamsF32 ep{};
+    ep.n_aux = op.n_aux;
+    ep.n_out = op.n_out;
+    ep.ldp = ldp;
+    for (int a = 0; a < op.n_aux; ++a) ep.aux[a] = xplane(op.aux[a], &ep.aux_ld[a]);
+    for (int j = 0; j < op.n_out; ++j) {
+      const int v = op.out[j];
+      int ld = ldp;
+      float* x = xplane(v, &ld);
+      ep.out_x[j] = (needx[v] || !role[v]) ? x : nullptr;
+      ep.out_hi[j] = (role[v] & 1) ? hi(v) : nullptr;
+      ep.out_lo[j] = (role[v] & 1) ? lo(v) : nullptr;
+      ep.out_hiT[j] = (role[v] & 2) ? hiT(v) : nullptr;
+      ep.out_loT[j] = (role[v] & 2) ? loT(v) : nullptr;
+      ep.out_ld[j] = ld;
+      ep.alpha[j] = op.alpha[j];
+      ep.gamma[j] = op.gamma[j];
+      for (int a = 0; a < kMaxAux; ++a) ep.beta[j][a] = op.beta[j][a];
+    }
+    int rc;
+    if (op.gemm) {
+      const int l = lr[i].first, r = lr[i].second;
+      rc = launch_gemm_tf32x3(hi(l), lo(l), hiT(r), loT(r), d, ldp, ep, s);
+    } else {
+      rc = launch_axpby_f32(d, ep, s);
+    }
+    if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    ++nl;
+  }
+  *launches = nl;
+  return NSERIES_OK;
 }
 
 // Execute a compiled program on the stream.
@@ -219,10 +334,15 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   if (!A || !S || d < 1 || k < 1) return NSERIES_ERR_INVALID_ARG;
   if (dt != NSERIES_F64 && dt != NSERIES_F32) return NSERIES_ERR_INVALID_ARG;
   if (A == S || (R_out && (A == R_out || S == R_out))) return NSERIES_ERR_ALIAS;
-  if (dt == NSERIES_F32) return NSERIES_ERR_INVALID_ARG;   // fp32 engine: see DESIGN.md status
   nseries_plan p;
   nseries_status st = resolve_plan(plan, k, flags, &p);
   if (st != NSERIES_OK) return st;
+  if (dt == NSERIES_F32) {
+    // fp32: radix-15 residual update in telescoping form R' = I - f + f R (same polynomial,
+    // PAPER.md:573; avoids the |Y| ~ kappa cancellation of I - Y' + A Y' in fp32 storage)
+    for (int i = 0; i < p.n_steps; ++i)
+      if (p.step[i] == 15) p.form[i] = 2;
+  }
   const bool want_R = R_out != nullptr;
   std::string key = plan_key(p, want_R);
   auto it = h->programs.find(key);
@@ -235,7 +355,7 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   const Program& P = it->second;
   cudaSetDevice(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = ensure_ws(h, (size_t)P.n_slots * d * d * elem_size(dt));
+  st = ensure_ws(h, dt == NSERIES_F64 ? (size_t)P.n_slots * d * d * sizeof(double) : f32_ws_bytes(P, d));
   if (st != NSERIES_OK) return st;
   if (P.needs_identity) {
     st = ensure_identity(h, d, dt, s);
@@ -244,7 +364,10 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
   if (timing) cudaEventRecord(h->ev0, s);
   int launches = 0;
-  st = run_program(h, P, A, S, R_out, d, dt, s, &launches);
+  st = dt == NSERIES_F64
+           ? run_program(h, P, A, S, R_out, d, dt, s, &launches)
+           : run_program_f32(h, P, static_cast<const float*>(A), static_cast<float*>(S),
+                             static_cast<float*>(R_out), d, s, &launches);
   if (st != NSERIES_OK) return st;
   h->stats.products = P.products;
   h->stats.launches = launches;
@@ -387,14 +510,33 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
   ep.alpha[0] = 1.0;
   cudaSetDevice(h->device);
   int rc;
-  if (dt == NSERIES_F64)
+  int launches = 1;
+  if (dt == NSERIES_F64) {
     rc = launch_gemm_f64(static_cast<const double*>(X), static_cast<const double*>(Y), d, ep,
                          stream);
-  else
-    return NSERIES_ERR_INVALID_ARG;
+  } else {
+    const int ldp = padded_ld(d);
+    const size_t plane = (size_t)d * ldp;
+    nseries_status st = ensure_ws(h, 4 * plane * sizeof(float));
+    if (st != NSERIES_OK) return st;
+    float* w = static_cast<float*>(h->ws);
+    rc = launch_split_f32(static_cast<const float*>(X), d, w, w + plane, nullptr, nullptr, ldp, d, false, stream);
+    if (!rc)
+      rc = launch_split_f32(static_cast<const float*>(Y), d, nullptr, nullptr, w + 2 * plane, w + 3 * plane, ldp,
+                            d, false, stream);
+    EpiParamsF32 e32{};
+    e32.ldp = ldp;
+    e32.n_aux = 0;
+    e32.n_out = 1;
+    e32.out_x[0] = static_cast<float*>(C);
+    e32.out_ld[0] = d;
+    e32.alpha[0] = 1.f;
+    if (!rc) rc = launch_gemm_tf32x3(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream);
+    launches = 3;
+  }
   h->stats = nseries_stats{};
   h->stats.products = 1;
-  h->stats.launches = 1;
+  h->stats.launches = launches;
   h->stats.n_ops = 1;
   return cuda_fail(h, (cudaError_t)rc);
 }

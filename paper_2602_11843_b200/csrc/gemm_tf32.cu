@@ -1,0 +1,469 @@
+// gemm_tf32.cu -- FP32 engine: 3xTF32 products on the 5th-generation tensor cores (sm_100a).
+//
+// acc = X * Y (d x d x d) with fp32 accuracy from three tcgen05.mma .kind::tf32 passes
+//   acc = Xhi*Yhi + (Xhi*Ylo + Xlo*Yhi)        (hi = rna_tf32(x), lo = rna_tf32(x - hi))
+// Operands live in HBM as tf32 "planes" (hi and lo, fp32 containers, leading dimension ldp,
+// a multiple of 32) written by the producing epilogue (or by the one-off split of the user's
+// A), so the mainloop is pure TMA -> SMEM -> tcgen05 with no conversion work (DESIGN.md
+// "FP32 engine").
+//
+// Tensor-core accumulation truncates toward zero (profiles/r01_tf32_accumulation_probe.txt),
+// which biases long accumulations (~0.3 ulp of the accumulator per instruction).  The K loop
+// is therefore split into chunks of CK k-blocks: each chunk accumulates in its own TMEM
+// buffer -- the two small cross terms first (while the accumulator is still small), then
+// hi*hi -- and the epilogue warps drain every chunk into fp32 register sums with IEEE adds
+// while the tensor core fills the next of NBUF buffers.
+//
+// CTA: 128x128 output tile, BK = 32 (one 128-byte swizzle row of fp32), 3-stage TMA ring of
+// {Xhi, Xlo, Yhi, Ylo} tiles (64 KB / stage).  Warp roles: w0 TMA producer, w1 MMA issuer,
+// w2 TMEM allocator, w4..w7 epilogue (TMEM lane quarter = warp % 4).
+// Both operands are K-major SWIZZLE_128B tiles (rows of 32 k-values, 8-row atoms, SBO = 1 KB,
+// +32 B per k-step).  .kind::tf32 with an MN-major B operand from SMEM returned all zeros on
+// this B200 (tools/tcgen05_probe.cu, profiles/r01_tcgen05_probe.txt), so the B role reads
+// TRANSPOSED planes Y^T (row n holds column n of Y); producing epilogues write them.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "internal.h"
+
+namespace nseries {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+constexpr int CK = 1;                        // k-blocks per accumulation chunk (Kc = 32)
+constexpr int NBUF = 2;                      // TMEM chunk buffers, each 2 x BN columns:
+                                             //  [small terms + hi*hi k-steps 0,1 | hi*hi k-steps 2,3]
+constexpr int kThreads = 256;
+constexpr uint32_t kTileBytes = BM * BK * 4;  // 16 KB per plane tile (A: 128x32, B: 32x128)
+constexpr uint32_t kStageBytes = 4 * kTileBytes;
+constexpr uint32_t kTmemCols = NBUF * 2 * BN; // 2 chunk buffers x 256 columns = 512
+
+struct Smem {
+  alignas(1024) uint8_t stage[STAGES][4][kTileBytes];   // [Xhi, Xlo, Yhi, Ylo]
+  alignas(8) uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tmem_full[NBUF];
+  uint64_t tmem_empty[NBUF];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)));
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(saddr(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  // bounded spin: a protocol bug traps instead of hanging the device
+  for (uint32_t i = 0; !mbar_try_wait(b, parity); ++i)
+    if (i > (1u << 30)) __trap();
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                            int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(saddr(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// SM100 shared-memory matrix descriptor (SWIZZLE_128B, version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // version = 1 (Blackwell)
+  d |= (uint64_t)2 << 61;          // layout = SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
+                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   saddr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+#ifdef NSERIES_TF32_DEBUG
+__device__ float* g_dbg = nullptr;
+#endif
+
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constant__ CUtensorMap mXl,
+                   const __grid_constant__ CUtensorMap mYh, const __grid_constant__ CUtensorMap mYl,
+                   int d, const __grid_constant__ EpiParamsF32 ep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntn = (d + BN - 1) / BN;
+  const int m0 = (blockIdx.x / ntn) * BM, n0 = (blockIdx.x % ntn) * BN;
+  const int KB = (d + BK - 1) / BK;
+  const int NC = (KB + CK - 1) / CK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
+    for (int b = 0; b < NBUF; ++b) { mbar_init(&sm.tmem_full[b], 1); mbar_init(&sm.tmem_empty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     saddr(&sm.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES, r = kb / STAGES;
+        if (r > 0) mbar_wait(&sm.empty[s], (r - 1) & 1);
+        mbar_expect_tx(&sm.full[s], kStageBytes);
+        const int k0 = kb * BK;
+        tma_load_2d(sm.stage[s][0], &mXh, &sm.full[s], k0, m0);
+        tma_load_2d(sm.stage[s][1], &mXl, &sm.full[s], k0, m0);
+        tma_load_2d(sm.stage[s][2], &mYh, &sm.full[s], k0, n0);   // Y^T rows n0..n0+127
+        tma_load_2d(sm.stage[s][3], &mYl, &sm.full[s], k0, n0);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      for (int c = 0; c < NC; ++c) {
+        const int b = c % NBUF, u = c / NBUF;   // buffer b, use count u
+        if (u > 0) mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
+        fence_after();
+        const uint32_t t_acc = tmem + b * 2 * BN, t_acc2 = t_acc + BN;
+        const int kb_end = min(KB, (c + 1) * CK);
+        for (int kb = c * CK; kb < kb_end; ++kb) {
+          const int s = kb % STAGES, r = kb / STAGES;
+          mbar_wait(&sm.full[s], r & 1);
+          fence_after();
+          const uint32_t xh = saddr(sm.stage[s][0]), xl = saddr(sm.stage[s][1]);
+          const uint32_t yh = saddr(sm.stage[s][2]), yl = saddr(sm.stage[s][3]);
+          const bool first_kb = (kb == c * CK);
+          // small cross terms first, hi*hi last (see header)
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint64_t a_h = smem_desc(xh + 32 * ks, 16, 1024), a_l = smem_desc(xl + 32 * ks, 16, 1024);
+            const uint64_t b_h = smem_desc(yh + 32 * ks, 16, 1024), b_l = smem_desc(yl + 32 * ks, 16, 1024);
+            mma_tf32(t_acc, a_h, b_l, (first_kb && ks == 0) ? 0u : 1u);
+            mma_tf32(t_acc, a_l, b_h, 1u);
+          }
+          // hi*hi split over two accumulators: each truncating accumulation step then sees at
+          // most half a chunk in its accumulator (bias ~ halves)
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint64_t a_h = smem_desc(xh + 32 * ks, 16, 1024);
+            const uint64_t b_h = smem_desc(yh + 32 * ks, 16, 1024);
+            if (ks < BK / 16) mma_tf32(t_acc, a_h, b_h, 1u);
+            else mma_tf32(t_acc2, a_h, b_h, (first_kb && ks == BK / 16) ? 0u : 1u);
+          }
+          mma_commit(&sm.empty[s]);            // frees the smem stage once these MMAs finish
+        }
+        mma_commit(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: drain chunks into fp32 registers, then the fused outputs
+    const int q = warp & 3;                    // TMEM lane quarter
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float acc[BN];
+#pragma unroll
+    for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+    for (int c = 0; c < NC; ++c) {
+      const int b = c % NBUF, u = c / NBUF;
+      mbar_wait(&sm.tmem_full[b], u & 1);
+      fence_after();
+      const uint32_t t_acc = tmem + lane_off + b * 2 * BN;
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) {
+        float v[32], w[32];
+        tmem_ld32(t_acc + 32 * j, v);
+        tmem_ld32(t_acc + BN + 32 * j, w);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[32 * j + i] += v[i] + w[i];
+      }
+      fence_before();
+      if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
+    }
+    // fused epilogue: row r of the tile, columns n0 .. n0+127
+    const int r = m0 + q * 32 + lane;
+    if (r < d) {
+#pragma unroll
+      for (int j0 = 0; j0 < BN; j0 += 4) {
+        const int c0 = n0 + j0;
+        if (c0 >= d) break;
+        const bool full4 = c0 + 4 <= d;
+        // linear combinations in binary64 (coefficients exact, one rounding per output)
+        double av[kMaxAux][4];
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x) {
+          if (x < ep.n_aux) {
+            const float* p = ep.aux[x] + (size_t)r * ep.aux_ld[x] + c0;
+            if (full4 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+              float4 t4 = *reinterpret_cast<const float4*>(p);
+              av[x][0] = t4.x; av[x][1] = t4.y; av[x][2] = t4.z; av[x][3] = t4.w;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) av[x][e] = (c0 + e < d) ? p[e] : 0.f;
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 0; o < kMaxOut; ++o) {
+          if (o >= ep.n_out) break;
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            double t = ep.alpha[o] * (double)acc[j0 + e];
+#pragma unroll
+            for (int x = 0; x < kMaxAux; ++x)
+              if (x < ep.n_aux) t = fma(ep.beta[o][x], av[x][e], t);
+            if (r == c0 + e) t += ep.gamma[o];
+            v[e] = (float)t;
+          }
+          if (ep.out_hiT[o]) {
+            // transposed operand planes: element (r, c) -> [c][r]; lanes hold consecutive r
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (c0 + e >= d) break;
+              const float hi = rna_tf32(v[e]);
+              ep.out_hiT[o][(size_t)(c0 + e) * ep.ldp + r] = hi;
+              ep.out_loT[o][(size_t)(c0 + e) * ep.ldp + r] = rna_tf32(v[e] - hi);
+            }
+          }
+          float* planes[3] = {ep.out_x[o], ep.out_hi[o], ep.out_lo[o]};
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) {
+            float* base = planes[pl];
+            if (!base) continue;
+            float w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float hi = rna_tf32(v[e]);
+              w[e] = pl == 0 ? v[e] : (pl == 1 ? hi : rna_tf32(v[e] - hi));
+            }
+            float* p = base + (size_t)r * (pl == 0 ? ep.out_ld[o] : ep.ldp) + c0;
+            if (full4 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+              *reinterpret_cast<float4*>(p) = make_float4(w[0], w[1], w[2], w[3]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (c0 + e < d) p[e] = w[e];
+            }
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// split x (ld_in) into tf32 planes hi/lo and/or transposed planes hiT/loT (ld_out);
+// identity != 0 splits I instead of x.  32x32 tiles through shared memory keep both the
+// row-major and the transposed writes coalesced.
+__global__ void split_planes_kernel(const float* __restrict__ x, int ld_in, float* __restrict__ hi,
+                                    float* __restrict__ lo, float* __restrict__ hiT,
+                                    float* __restrict__ loT, int ld_out, int d, int identity) {
+  __shared__ float th[32][33], tl[32][33];
+  const int tiles = (d + 31) / 32;
+  for (int t = blockIdx.x; t < tiles * tiles; t += gridDim.x) {
+    const int r0 = (t / tiles) * 32, c0 = (t % tiles) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int r = r0 + i, c = c0 + threadIdx.x;
+      float h = 0.f, l = 0.f;
+      if (r < d && c < d) {
+        const float v = identity ? (r == c ? 1.f : 0.f) : x[(size_t)r * ld_in + c];
+        h = rna_tf32(v);
+        l = rna_tf32(v - h);
+        if (hi) { hi[(size_t)r * ld_out + c] = h; lo[(size_t)r * ld_out + c] = l; }
+      }
+      th[i][threadIdx.x] = h;
+      tl[i][threadIdx.x] = l;
+    }
+    __syncthreads();
+    if (hiT) {
+      for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;   // write row c of the transpose
+        if (r < d && c < d) {
+          hiT[(size_t)c * ld_out + r] = th[threadIdx.x][i];
+          loT[(size_t)c * ld_out + r] = tl[threadIdx.x][i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void axpby_f32_kernel(int d, const __grid_constant__ EpiParamsF32 ep) {
+  const size_t n = (size_t)d * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / d), c = (int)(i % d);
+    for (int o = 0; o < ep.n_out; ++o) {
+      double t = 0.0;
+      for (int x = 0; x < ep.n_aux; ++x) t = fma(ep.beta[o][x], (double)ep.aux[x][(size_t)r * ep.aux_ld[x] + c], t);
+      if (r == c) t += ep.gamma[o];
+      const float v = (float)t;
+      const float h = rna_tf32(v), l = rna_tf32(v - h);
+      if (ep.out_x[o]) ep.out_x[o][(size_t)r * ep.out_ld[o] + c] = v;
+      if (ep.out_hi[o]) { ep.out_hi[o][(size_t)r * ep.ldp + c] = h; ep.out_lo[o][(size_t)r * ep.ldp + c] = l; }
+      if (ep.out_hiT[o]) { ep.out_hiT[o][(size_t)c * ep.ldp + r] = h; ep.out_loT[o][(size_t)c * ep.ldp + r] = l; }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host: tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// role 0: A operand box {32 k, 128 rows}; role 1: B operand box {32 n, 32 k}
+int make_map(CUtensorMap* m, const float* base, int d, int ld, int role) {
+  auto enc = get_encode();
+  if (!enc) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)d};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32u, role == 0 ? (cuuint32_t)BM : (cuuint32_t)BK};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+struct MapCache {
+  std::mutex mu;
+  std::map<std::tuple<const void*, int, int, int>, CUtensorMap> maps;
+  int get(const float* p, int d, int ld, int role, CUtensorMap* out) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple((const void*)p, d, ld, role);
+    auto it = maps.find(key);
+    if (it == maps.end()) {
+      CUtensorMap m;
+      int rc = make_map(&m, p, d, ld, role);
+      if (rc) return rc;
+      it = maps.emplace(key, m).first;
+    }
+    *out = it->second;
+    return 0;
+  }
+};
+MapCache g_maps;
+
+}  // namespace
+
+int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
+                       const EpiParamsF32& ep, void* stream) {
+  CUtensorMap mxh, mxl, myh, myl;
+  int rc = g_maps.get(Xh, d, ldp, 0, &mxh);
+  if (!rc) rc = g_maps.get(Xl, d, ldp, 0, &mxl);
+  if (!rc) rc = g_maps.get(Yh, d, ldp, 0, &myh);   // transposed planes, same K-major box
+  if (!rc) rc = g_maps.get(Yl, d, ldp, 0, &myl);
+  if (rc) return rc;
+  const size_t smem = sizeof(Smem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  const int tiles = ((d + BM - 1) / BM) * ((d + BN - 1) / BN);
+  gemm_tf32x3_kernel<<<tiles, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(mxh, mxl, myh, myl, d, ep);
+  return (int)cudaGetLastError();
+}
+
+int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT, float* loT, int ld_out,
+                     int d, bool identity, void* stream) {
+  const int tiles = (d + 31) / 32;
+  const int blocks = std::min(tiles * tiles, 148 * 8);
+  split_planes_kernel<<<blocks, dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(
+      x, ld_in, hi, lo, hiT, loT, ld_out, d, identity ? 1 : 0);
+  return (int)cudaGetLastError();
+}
+
+int launch_axpby_f32(int d, const EpiParamsF32& ep, void* stream) {
+  const size_t n = (size_t)d * d;
+  int blocks = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+  axpby_f32_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(d, ep);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace nseries

@@ -92,6 +92,31 @@ int launch_batched(nseries_dtype dt, const void* A, int64_t strideA, const void*
                    void* S, int64_t strideS, void* const* S_ptrs, int batch, int d,
                    const BatchedProgram& prog, void* stream);
 
+// fp32 engine (gemm_tf32.cu): operands as tf32 hi/lo planes with leading dimension ldp
+// (multiple of 32): X role row-major (hi, lo), Y role transposed (hiT, loT); epilogue planes:
+// x (fp32 value), hi, lo, hiT, loT (any may be null).
+struct EpiParamsF32 {
+  int n_aux, n_out;
+  const float* aux[kMaxAux];
+  int aux_ld[kMaxAux];
+  float* out_x[kMaxOut];
+  float* out_hi[kMaxOut];
+  float* out_lo[kMaxOut];
+  float* out_hiT[kMaxOut];      // transposed operand planes (B role)
+  float* out_loT[kMaxOut];
+  int out_ld[kMaxOut];          // leading dimension of out_x (operand planes use ldp)
+  int ldp;
+  double alpha[kMaxOut];          // binary64: the epilogue combines in double, rounds once
+  double beta[kMaxOut][kMaxAux];
+  double gamma[kMaxOut];
+};
+int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
+                       const EpiParamsF32& ep, void* stream);
+int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT, float* loT, int ld_out,
+                     int d, bool identity, void* stream);
+int launch_axpby_f32(int d, const EpiParamsF32& ep, void* stream);
+inline int padded_ld(int d) { return (d + 31) / 32 * 32; }
+
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);
 int launch_axpby_f64(int d, const EpiParams& ep, void* stream);

@@ -216,3 +216,57 @@ def test_config5_probes(h):
     ref, used = O.series_sum(A, 10000, V, norm_bound=0.99 + 1e-9, tail_tol=1e-20)
     got = O.matvec(S.cpu().numpy(), V)
     assert O.rel_fro(got, ref) <= TOL64
+
+
+# ---------------------------------------------------------------- fp32 (3xTF32 on tcgen05)
+
+TOL32 = 2e-5
+
+
+@pytest.mark.parametrize("d", [1, 2, 7, 16, 31, 33, 64, 100, 130, 257])
+@pytest.mark.parametrize("steps", [[9, 9], [5, 5, 5], [2] * 6, [15, 15], [15, 1, 5], [9, 1, 2], [1], [2]])
+def test_parity_small_f32(h, d, steps):
+    A = inputs.random_matrix(d, 300 + d, 0.7).astype(np.float32)
+    S, _, _ = _run(h, A.astype(np.float64), steps, dtype=torch.float32)
+    ref = _oracle_full(A.astype(np.float64), steps)     # oracle on fl32(A), the GPU's exact input
+    assert O.rel_fro(S, ref) <= TOL32, (d, steps)
+
+
+@pytest.mark.parametrize("steps", [[9, 9], [15, 15], [2] * 5, [1, 2]])
+@pytest.mark.parametrize("extra", [0, P.NSERIES_ELIDE_TRIVIAL, P.NSERIES_RFORM_TELESCOPE])
+def test_parity_f32_flags_and_R(h, steps, extra):
+    d = 72
+    A = inputs.random_matrix(d, 9, 0.8).astype(np.float32)
+    S, R, _ = _run(h, A.astype(np.float64), steps, flags=extra, want_R=True, dtype=torch.float32)
+    Sref, Rref = _oracle_full(A.astype(np.float64), steps, want_R=True)
+    assert O.rel_fro(S, Sref) <= TOL32
+    if not (extra & P.NSERIES_ELIDE_TRIVIAL):
+        scale = float(np.sqrt(np.sum(np.asarray(Sref, dtype=LD) ** 2)))
+        assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-5
+
+
+@pytest.mark.parametrize("d", [5, 128, 300, 1024, 2048])
+def test_matmul_engine_f32(h, d):
+    # one 3xTF32 product vs the exact product of the fp32 inputs (<= 5e-7 budget)
+    rng = np.random.default_rng(d + 7)
+    X = rng.standard_normal((d, d)).astype(np.float32)
+    Y = rng.standard_normal((d, d)).astype(np.float32)
+    Xt, Yt = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+    C = torch.empty_like(Xt)
+    P.nseries_matmul(h, Xt, Yt, C, d)
+    torch.cuda.synchronize()
+    cols = np.arange(d) if d <= 300 else rng.choice(d, 16, replace=False)
+    ref = O.matvec(X.astype(np.float64), Y[:, cols].astype(np.float64))
+    assert O.rel_fro(C.cpu().numpy()[:, cols], ref) <= 5e-7
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("steps", [[15, 15, 15], [9, 9, 9, 9], [2] * 12])
+def test_config3_probes_f32(h, steps):
+    A_dev, _, _ = inputs.cfg3(device="cuda")
+    A32 = A_dev.float()
+    A = A32.double().cpu().numpy()                     # fl32(A), exactly what the GPU sees
+    V, _ = inputs.probe_block(A.shape[0], 2, n_unit=1, n_gauss=1)
+    S, _, _ = _run(h, A, steps, dtype=torch.float32)
+    # at the fp32 tolerance the S_k oracle also bounds the radix-15 deviation (1.7e-8)
+    assert _probe_parity(S.astype(np.float64), A, steps, V, 15 in steps) <= TOL32
