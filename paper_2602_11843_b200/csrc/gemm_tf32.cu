@@ -40,7 +40,9 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
 constexpr int CK = 1;                        // k-blocks per accumulation chunk (Kc = 32)
 constexpr int NBUF = 2;                      // TMEM chunk buffers, each 2 x BN columns:
                                              //  [small terms + hi*hi k-steps 0,1 | hi*hi k-steps 2,3]
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, 64 columns each
+constexpr int EC = BN / 2;                   // columns per epilogue thread
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr uint32_t kTileBytes = BM * BK * 4;  // 16 KB per plane tile (A: 128x32, B: 32x128)
 constexpr uint32_t kStageBytes = 4 * kTileBytes;
 constexpr uint32_t kTmemCols = NBUF * 2 * BN; // 2 chunk buffers x 256 columns = 512
@@ -121,6 +123,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// issue a 32-column TMEM load without waiting (pair with tmem_wait_ld before use)
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   asm volatile(
@@ -158,10 +176,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   const int m0 = (blockIdx.x / ntn) * BM, n0 = (blockIdx.x % ntn) * BN;
   const int KB = (d + BK - 1) / BK;
   const int NC = (KB + CK - 1) / CK;
+#ifdef NSERIES_TF32_DEBUG
+  const long long t_kernel0 = clock64();
+  long long t_drained = 0;
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
-    for (int b = 0; b < NBUF; ++b) { mbar_init(&sm.tmem_full[b], 1); mbar_init(&sm.tmem_empty[b], 4); }
+    for (int b = 0; b < NBUF; ++b) { mbar_init(&sm.tmem_full[b], 1); mbar_init(&sm.tmem_empty[b], kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -192,15 +214,31 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
     if (lane == 0) {
+#ifdef NSERIES_TF32_DEBUG
+      long long tstart = clock64();
+      if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
+#endif
       for (int c = 0; c < NC; ++c) {
         const int b = c % NBUF, u = c / NBUF;   // buffer b, use count u
+#ifdef NSERIES_TF32_DEBUG
+        long long t0 = clock64();
+#endif
         if (u > 0) mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
+#ifdef NSERIES_TF32_DEBUG
+        if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
+#endif
         fence_after();
         const uint32_t t_acc = tmem + b * 2 * BN, t_acc2 = t_acc + BN;
         const int kb_end = min(KB, (c + 1) * CK);
         for (int kb = c * CK; kb < kb_end; ++kb) {
           const int s = kb % STAGES, r = kb / STAGES;
+#ifdef NSERIES_TF32_DEBUG
+          long long t1 = clock64();
+#endif
           mbar_wait(&sm.full[s], r & 1);
+#ifdef NSERIES_TF32_DEBUG
+          if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
+#endif
           fence_after();
           const uint32_t xh = saddr(sm.stage[s][0]), xl = saddr(sm.stage[s][1]);
           const uint32_t yh = saddr(sm.stage[s][2]), yl = saddr(sm.stage[s][3]);
@@ -226,100 +264,102 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         }
         mma_commit(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
       }
+#ifdef NSERIES_TF32_DEBUG
+      if (g_dbg) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 2, 1ull);
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 3, (unsigned long long)(clock64() - tstart));
+      }
+#endif
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: drain chunks into fp32 registers, then the fused outputs
-    const int q = warp & 3;                    // TMEM lane quarter
+    const int q = warp & 3;                    // TMEM lane quarter (hardware: warp % 4)
+    const int cb = ((warp - 4) >> 2) * EC;     // this warp's column half of the tile
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float acc[BN];
+    float acc[EC];
 #pragma unroll
-    for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+    for (int i = 0; i < EC; ++i) acc[i] = 0.f;
     for (int c = 0; c < NC; ++c) {
       const int b = c % NBUF, u = c / NBUF;
       mbar_wait(&sm.tmem_full[b], u & 1);
       fence_after();
-      const uint32_t t_acc = tmem + lane_off + b * 2 * BN;
+      const uint32_t t_acc = tmem + lane_off + b * 2 * BN + cb;
 #pragma unroll
-      for (int j = 0; j < BN / 32; ++j) {
-        float v[32], w[32];
-        tmem_ld32(t_acc + 32 * j, v);
-        tmem_ld32(t_acc + BN + 32 * j, w);
+      for (int j = 0; j < EC / 32; ++j) {
+        uint32_t v[32], w[32];
+        tmem_ld32_async(t_acc + 32 * j, v);
+        tmem_ld32_async(t_acc + BN + 32 * j, w);
+        tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[32 * j + i] += v[i] + w[i];
+        for (int i = 0; i < 32; ++i) acc[32 * j + i] += __uint_as_float(v[i]) + __uint_as_float(w[i]);
       }
       fence_before();
       if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
     }
-    // fused epilogue: row r of the tile, columns n0 .. n0+127
-    const int r = m0 + q * 32 + lane;
-    if (r < d) {
+#ifdef NSERIES_TF32_DEBUG
+    t_drained = clock64();
+#endif
+    // ---- fused epilogue, staged through shared memory (the TMA ring is idle now: every MMA
+    // has completed and every stage was consumed).  acc tile [128][129] then per output a
+    // value tile [128][129]; the +1 pad keeps row- and column-wise accesses conflict-free.
+    float* tile = reinterpret_cast<float*>(&sm.stage[0][0][0]);
+    float* vt = tile + BM * (BN + 1);
+    const int rl = q * 32 + lane;
 #pragma unroll
-      for (int j0 = 0; j0 < BN; j0 += 4) {
-        const int c0 = n0 + j0;
-        if (c0 >= d) break;
-        const bool full4 = c0 + 4 <= d;
-        // linear combinations in binary64 (coefficients exact, one rounding per output)
-        double av[kMaxAux][4];
+    for (int i = 0; i < EC; ++i) tile[rl * (BN + 1) + cb + i] = acc[i];
+    const int et = threadIdx.x - 128;          // 0..255 among the epilogue warps
+    const int ew = et >> 5;                    // epilogue warp 0..7
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+    for (int o = 0; o < ep.n_out; ++o) {
+      // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns)
+      for (int rr = ew; rr < BM; rr += kEpiWarps) {
+        const int r = m0 + rr;
+        if (r >= d) break;
 #pragma unroll
-        for (int x = 0; x < kMaxAux; ++x) {
-          if (x < ep.n_aux) {
-            const float* p = ep.aux[x] + (size_t)r * ep.aux_ld[x] + c0;
-            if (full4 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-              float4 t4 = *reinterpret_cast<const float4*>(p);
-              av[x][0] = t4.x; av[x][1] = t4.y; av[x][2] = t4.z; av[x][3] = t4.w;
-            } else {
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          const int cl = cc * 32 + lane, c = n0 + cl;
+          if (c >= d) break;
+          double t = ep.alpha[o] * (double)tile[rr * (BN + 1) + cl];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) av[x][e] = (c0 + e < d) ? p[e] : 0.f;
-            }
+          for (int x = 0; x < kMaxAux; ++x)
+            if (x < ep.n_aux) t = fma(ep.beta[o][x], (double)ep.aux[x][(size_t)r * ep.aux_ld[x] + c], t);
+          if (r == c) t += ep.gamma[o];
+          const float v = (float)t;
+          const float hi = rna_tf32(v), lo = rna_tf32(v - hi);
+          if (ep.out_x[o]) ep.out_x[o][(size_t)r * ep.out_ld[o] + c] = v;
+          if (ep.out_hi[o]) {
+            ep.out_hi[o][(size_t)r * ep.ldp + c] = hi;
+            ep.out_lo[o][(size_t)r * ep.ldp + c] = lo;
           }
+          vt[rr * (BN + 1) + cl] = v;
         }
+      }
+      if (ep.out_hiT[o]) {
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+        // column pass: transposed operand planes, lanes along rows of the tile
+        for (int cl = ew; cl < BN; cl += kEpiWarps) {
+          const int c = n0 + cl;
+          if (c >= d) break;
 #pragma unroll
-        for (int o = 0; o < kMaxOut; ++o) {
-          if (o >= ep.n_out) break;
-          float v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            double t = ep.alpha[o] * (double)acc[j0 + e];
-#pragma unroll
-            for (int x = 0; x < kMaxAux; ++x)
-              if (x < ep.n_aux) t = fma(ep.beta[o][x], av[x][e], t);
-            if (r == c0 + e) t += ep.gamma[o];
-            v[e] = (float)t;
-          }
-          if (ep.out_hiT[o]) {
-            // transposed operand planes: element (r, c) -> [c][r]; lanes hold consecutive r
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              if (c0 + e >= d) break;
-              const float hi = rna_tf32(v[e]);
-              ep.out_hiT[o][(size_t)(c0 + e) * ep.ldp + r] = hi;
-              ep.out_loT[o][(size_t)(c0 + e) * ep.ldp + r] = rna_tf32(v[e] - hi);
-            }
-          }
-          float* planes[3] = {ep.out_x[o], ep.out_hi[o], ep.out_lo[o]};
-#pragma unroll
-          for (int pl = 0; pl < 3; ++pl) {
-            float* base = planes[pl];
-            if (!base) continue;
-            float w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float hi = rna_tf32(v[e]);
-              w[e] = pl == 0 ? v[e] : (pl == 1 ? hi : rna_tf32(v[e] - hi));
-            }
-            float* p = base + (size_t)r * (pl == 0 ? ep.out_ld[o] : ep.ldp) + c0;
-            if (full4 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-              *reinterpret_cast<float4*>(p) = make_float4(w[0], w[1], w[2], w[3]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (c0 + e < d) p[e] = w[e];
-            }
+          for (int rc = 0; rc < BM / 32; ++rc) {
+            const int rr = rc * 32 + lane, r = m0 + rr;
+            if (r >= d) break;
+            const float v = vt[rr * (BN + 1) + cl];
+            const float hi = rna_tf32(v);
+            ep.out_hiT[o][(size_t)c * ep.ldp + r] = hi;
+            ep.out_loT[o][(size_t)c * ep.ldp + r] = rna_tf32(v - hi);
           }
         }
       }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
     }
   }
+#ifdef NSERIES_TF32_DEBUG
+  if (warp == 4 && lane == 0 && g_dbg) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 5, (unsigned long long)(clock64() - t_drained));
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 6, (unsigned long long)(t_drained - t_kernel0));
+  }
+#endif
   fence_before();
   __syncthreads();
   if (warp == 2) {
