@@ -33,6 +33,9 @@ PLANS = {"x15^3": ([15, 15, 15], 3375), "x9^4": ([9, 9, 9, 9], 6561), "x2^12": (
 # this pool's B200 (tools/peak_fp64.cu -> profiles/peaks_r01_fp64_microbench.json).
 FP64_PEAK_TFLOPS = 37.161
 FP64_PEAK_SOURCE = "measured: DMMA m8n8k4 register loop, tools/peak_fp64.cu (profiles/peaks_r01_fp64_microbench.json)"
+# TF32 dense peak: measured bf16 burst (MEASURED_PEAKS.json, 1631.3 TF) x the guide's nominal
+# tf32/bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md) -- "of measured x nominal ratio"
+TF32_PEAK_TFLOPS = 1631.3 * 1.1 / 2.25
 REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
@@ -242,6 +245,20 @@ def run_native(args):
             p = per_plan[name]
             p["time_ratio_vs_binary"] = p["ms_per_eval"] / b["ms_per_eval"]
             p["target_ratio"] = (p["products"] / b["products"]) / 0.95
+        # fp32 (3xTF32 on tcgen05) on fl32(A): same plans, tensor-pipe rate = 3 x algorithmic
+        A32 = A.float().contiguous()
+        S32 = torch.empty_like(A32)
+        for name, (stp, kk) in PLANS.items():
+            fl = P.NSERIES_ALLOW_APPROX if 15 in stp else 0
+            n = max(2, args.steps // 2)
+            pms, pplan, _ = time_plan(P, h, A32, S32, stp, kk, n, 2, fl, stream, world)
+            pstep = pms / n
+            alg = pplan.products * flop_per_product / (pstep * 1e-3) / 1e12
+            per_plan[name + " fp32"] = {"k": kk, "products": pplan.products, "ms_per_eval": pstep,
+                                        "evals_per_s": world * 1e3 / pstep, "tflops": alg,
+                                        "tf32_tensor_tflops": 3 * alg,
+                                        "tf32_frac_of_peak": 3 * alg / TF32_PEAK_TFLOPS}
+        del A32, S32
 
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     A_host = A.cpu().pin_memory()

@@ -36,25 +36,42 @@
 namespace nseries {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
-constexpr int CK = 1;                        // k-blocks per accumulation chunk (Kc = 32)
-constexpr int NBUF = 2;                      // TMEM chunk buffers, each 2 x BN columns:
-                                             //  [small terms + hi*hi k-steps 0,1 | hi*hi k-steps 2,3]
-constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, 64 columns each
+#ifndef NSERIES_TF32_BN
+#define NSERIES_TF32_BN 256
+#define NSERIES_TF32_BK 32
+#define NSERIES_TF32_STAGES 2
+#endif
+constexpr int BM = 128, BN = NSERIES_TF32_BN, BK = NSERIES_TF32_BK, STAGES = NSERIES_TF32_STAGES;
+// BK = 16 fp32 = 64-byte rows -> SWIZZLE_64B tiles (8-row atoms of 512 B).  Each 16-wide K
+// chunk is one accumulation unit; NBUF = 4 chunk accumulators keep 4 chunks (24 MMAs) queued
+// ahead of the drain round trip (commit -> epilogue tcgen05.ld -> arrive), which a 2-deep
+// buffer (128x256 tiles) could not hide (tools/tf32_timing.cu).
+constexpr int KSC = 2;                       // k-steps (of 8) per accumulation chunk (Kc = 16)
+constexpr int CPS = (BK / 8) / KSC;          // chunks per smem stage
+constexpr int NBUF = 512 / BN;               // TMEM chunk accumulators of BN columns
+constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, BN/2 columns each
 constexpr int EC = BN / 2;                   // columns per epilogue thread
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr uint32_t kTileBytes = BM * BK * 4;  // 16 KB per plane tile (A: 128x32, B: 32x128)
-constexpr uint32_t kStageBytes = 4 * kTileBytes;
-constexpr uint32_t kTmemCols = NBUF * 2 * BN; // 2 chunk buffers x 256 columns = 512
+constexpr uint32_t kATileBytes = BM * BK * 4;   // 8 KB  (128 rows x 16 k)
+constexpr uint32_t kBTileBytes = BN * BK * 4;   // 8 KB (128 rows of Y^T x 16 k)
+constexpr uint32_t kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
+constexpr uint32_t kTmemCols = NBUF * BN;       // 512
+constexpr uint32_t kSwizzleLayout = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / _64B
+constexpr uint32_t kAtomBytes = 8 * BK * 4;     // 8 rows x 64 B = 512 B (SBO)
+constexpr int kStageLd = EC + 1;                // epilogue staging row (floats)
 
 struct Smem {
-  alignas(1024) uint8_t stage[STAGES][4][kTileBytes];   // [Xhi, Xlo, Yhi, Ylo]
+  alignas(1024) uint8_t xh[STAGES][kATileBytes];
+  alignas(1024) uint8_t xl[STAGES][kATileBytes];
+  alignas(1024) uint8_t yh[STAGES][kBTileBytes];
+  alignas(1024) uint8_t yl[STAGES][kBTileBytes];
   alignas(8) uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tmem_full[NBUF];
   uint64_t tmem_empty[NBUF];
   uint32_t tmem_base;
 };
+static_assert(2 * BM * kStageLd * 4 <= STAGES * kStageBytes, "epilogue staging must fit the TMA ring");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -78,6 +95,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// non-blocking probe: issue early, consume the predicate later (hides the ~100-cycle
+// barrier round trip behind MMA issue)
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(saddr(b)), "r"(parity)
+      : "memory");
+  return ok;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   // bounded spin: a protocol bug traps instead of hanging the device
   for (uint32_t i = 0; !mbar_try_wait(b, parity); ++i)
@@ -96,18 +124,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// SM100 shared-memory matrix descriptor (SWIZZLE_128B, version 1).
+// SM100 shared-memory matrix descriptor (K-major, swizzled, version 1).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;          // version = 1 (Blackwell)
-  d |= (uint64_t)2 << 61;          // layout = SWIZZLE_128B
+  d |= (uint64_t)kSwizzleLayout << 61;
   return d;
 }
 
-// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128.
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = BN.
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
@@ -155,6 +183,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// packed fp32 add (SASS FADD2): acc[0:1] += (x, y), IEEE round-to-nearest
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float x, float y) {
+  unsigned long long ua, ub;
+  ua = ((unsigned long long)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+  ub = ((unsigned long long)__float_as_uint(y) << 32) | __float_as_uint(x);
+  unsigned long long uc;
+  asm("add.rn.f32x2 %0, %1, %2;\n" : "=l"(uc) : "l"(ua), "l"(ub));
+  a0 = __uint_as_float((uint32_t)uc);
+  a1 = __uint_as_float((uint32_t)(uc >> 32));
+}
+
 __device__ __forceinline__ float rna_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
@@ -175,7 +214,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   const int ntn = (d + BN - 1) / BN;
   const int m0 = (blockIdx.x / ntn) * BM, n0 = (blockIdx.x % ntn) * BN;
   const int KB = (d + BK - 1) / BK;
-  const int NC = (KB + CK - 1) / CK;
+  const int NC = KB * CPS;                   // accumulation chunks
 #ifdef NSERIES_TF32_DEBUG
   const long long t_kernel0 = clock64();
   long long t_drained = 0;
@@ -203,12 +242,16 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       for (int kb = 0; kb < KB; ++kb) {
         const int s = kb % STAGES, r = kb / STAGES;
         if (r > 0) mbar_wait(&sm.empty[s], (r - 1) & 1);
+#ifdef NSERIES_TF32_NO_TMA
+        mbar_arrive(&sm.full[s]);
+#else
         mbar_expect_tx(&sm.full[s], kStageBytes);
         const int k0 = kb * BK;
-        tma_load_2d(sm.stage[s][0], &mXh, &sm.full[s], k0, m0);
-        tma_load_2d(sm.stage[s][1], &mXl, &sm.full[s], k0, m0);
-        tma_load_2d(sm.stage[s][2], &mYh, &sm.full[s], k0, n0);   // Y^T rows n0..n0+127
-        tma_load_2d(sm.stage[s][3], &mYl, &sm.full[s], k0, n0);
+        tma_load_2d(sm.xh[s], &mXh, &sm.full[s], k0, m0);
+        tma_load_2d(sm.xl[s], &mXl, &sm.full[s], k0, m0);
+        tma_load_2d(sm.yh[s], &mYh, &sm.full[s], k0, n0);   // Y^T rows n0..n0+BN-1
+        tma_load_2d(sm.yl[s], &mYl, &sm.full[s], k0, n0);
+#endif
       }
     }
   } else if (warp == 1) {
@@ -218,51 +261,52 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       long long tstart = clock64();
       if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
 #endif
-      for (int c = 0; c < NC; ++c) {
-        const int b = c % NBUF, u = c / NBUF;   // buffer b, use count u
+      // The tensor pipe queues only a couple of MMAs, so any gap in issue longer than one MMA
+      // (64 cycles at N = 128) idles it.  Barrier state for the NEXT k-block / chunk is
+      // therefore probed with test_wait before this k-block's MMAs are issued and only
+      // waited on (rarely) afterwards; descriptors are built once per stage and advanced by
+      // adding the k-step offset to the start-address field.
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES, r = kb / STAGES;
 #ifdef NSERIES_TF32_DEBUG
-        long long t0 = clock64();
+        long long t1 = clock64();
 #endif
-        if (u > 0) mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
+        mbar_wait(&sm.full[s], r & 1);
 #ifdef NSERIES_TF32_DEBUG
-        if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
+        if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
 #endif
         fence_after();
-        const uint32_t t_acc = tmem + b * 2 * BN, t_acc2 = t_acc + BN;
-        const int kb_end = min(KB, (c + 1) * CK);
-        for (int kb = c * CK; kb < kb_end; ++kb) {
-          const int s = kb % STAGES, r = kb / STAGES;
+        const uint64_t dxh = smem_desc(saddr(sm.xh[s]), 16, kAtomBytes), dxl = smem_desc(saddr(sm.xl[s]), 16, kAtomBytes);
+        const uint64_t dyh = smem_desc(saddr(sm.yh[s]), 16, kAtomBytes), dyl = smem_desc(saddr(sm.yl[s]), 16, kAtomBytes);
+#pragma unroll
+        for (int h = 0; h < CPS; ++h) {
+          const int c = kb * CPS + h;
+          const int b = c % NBUF, u = c / NBUF;   // accumulator b, use count u
 #ifdef NSERIES_TF32_DEBUG
-          long long t1 = clock64();
+          long long t0 = clock64();
 #endif
-          mbar_wait(&sm.full[s], r & 1);
+          if (u > 0) mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
 #ifdef NSERIES_TF32_DEBUG
-          if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
+          if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
 #endif
           fence_after();
-          const uint32_t xh = saddr(sm.stage[s][0]), xl = saddr(sm.stage[s][1]);
-          const uint32_t yh = saddr(sm.stage[s][2]), yl = saddr(sm.stage[s][3]);
-          const bool first_kb = (kb == c * CK);
-          // small cross terms first, hi*hi last (see header)
+          const uint32_t t_acc = tmem + b * BN;
+          // small cross terms first (accumulator still small), hi*hi last; K-major swizzled
+          // tiles advance 32 B (8 tf32, +2 in the >>4 address field) per k-step
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint64_t a_h = smem_desc(xh + 32 * ks, 16, 1024), a_l = smem_desc(xl + 32 * ks, 16, 1024);
-            const uint64_t b_h = smem_desc(yh + 32 * ks, 16, 1024), b_l = smem_desc(yl + 32 * ks, 16, 1024);
-            mma_tf32(t_acc, a_h, b_l, (first_kb && ks == 0) ? 0u : 1u);
-            mma_tf32(t_acc, a_l, b_h, 1u);
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma_tf32(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
+            mma_tf32(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
           }
-          // hi*hi split over two accumulators: each truncating accumulation step then sees at
-          // most half a chunk in its accumulator (bias ~ halves)
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint64_t a_h = smem_desc(xh + 32 * ks, 16, 1024);
-            const uint64_t b_h = smem_desc(yh + 32 * ks, 16, 1024);
-            if (ks < BK / 16) mma_tf32(t_acc, a_h, b_h, 1u);
-            else mma_tf32(t_acc2, a_h, b_h, (first_kb && ks == BK / 16) ? 0u : 1u);
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma_tf32(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
           }
-          mma_commit(&sm.empty[s]);            // frees the smem stage once these MMAs finish
+          mma_commit(&sm.tmem_full[b]);        // chunk accumulator ready for the epilogue
         }
-        mma_commit(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
+        mma_commit(&sm.empty[s]);              // frees the smem stage once these MMAs finish
       }
 #ifdef NSERIES_TF32_DEBUG
       if (g_dbg) {
@@ -274,7 +318,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   } else if (warp >= 4) {
     // ---------------- epilogue: drain chunks into fp32 registers, then the fused outputs
     const int q = warp & 3;                    // TMEM lane quarter (hardware: warp % 4)
-    const int cb = ((warp - 4) >> 2) * EC;     // this warp's column half of the tile
+    const int half = (warp - 4) >> 2;          // this warp's column half of the tile
+    const int cb = half * EC;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     float acc[EC];
 #pragma unroll
@@ -283,75 +328,99 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       const int b = c % NBUF, u = c / NBUF;
       mbar_wait(&sm.tmem_full[b], u & 1);
       fence_after();
-      const uint32_t t_acc = tmem + lane_off + b * 2 * BN + cb;
+      const uint32_t t_acc = tmem + lane_off + b * BN + cb;
+#ifndef NSERIES_TF32_NO_DRAIN
 #pragma unroll
-      for (int j = 0; j < EC / 32; ++j) {
+      for (int j = 0; j < EC / 32; j += 2) {
         uint32_t v[32], w[32];
         tmem_ld32_async(t_acc + 32 * j, v);
-        tmem_ld32_async(t_acc + BN + 32 * j, w);
+        tmem_ld32_async(t_acc + 32 * (j + 1), w);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[32 * j + i] += __uint_as_float(v[i]) + __uint_as_float(w[i]);
+        for (int i = 0; i < 32; i += 2) {
+          fadd2(acc[32 * j + i], acc[32 * j + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          fadd2(acc[32 * (j + 1) + i], acc[32 * (j + 1) + i + 1], __uint_as_float(w[i]), __uint_as_float(w[i + 1]));
+        }
       }
+#endif
       fence_before();
       if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
     }
 #ifdef NSERIES_TF32_DEBUG
     t_drained = clock64();
 #endif
-    // ---- fused epilogue, staged through shared memory (the TMA ring is idle now: every MMA
-    // has completed and every stage was consumed).  acc tile [128][129] then per output a
-    // value tile [128][129]; the +1 pad keeps row- and column-wise accesses conflict-free.
-    float* tile = reinterpret_cast<float*>(&sm.stage[0][0][0]);
-    float* vt = tile + BM * (BN + 1);
+    // ---- fused epilogue, staged through shared memory one column half at a time (the TMA
+    // ring is idle: every MMA has completed and every stage was consumed).  Staging tiles
+    // [128][EC+1] (acc, then the output value); the +1 pad keeps row- and column-wise
+    // accesses conflict-free.
+    float* tile = reinterpret_cast<float*>(&sm.xh[0][0]);
+    float* vt = tile + BM * kStageLd;
     const int rl = q * 32 + lane;
-#pragma unroll
-    for (int i = 0; i < EC; ++i) tile[rl * (BN + 1) + cb + i] = acc[i];
     const int et = threadIdx.x - 128;          // 0..255 among the epilogue warps
     const int ew = et >> 5;                    // epilogue warp 0..7
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
-    for (int o = 0; o < ep.n_out; ++o) {
-      // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns)
-      for (int rr = ew; rr < BM; rr += kEpiWarps) {
-        const int r = m0 + rr;
-        if (r >= d) break;
+    for (int hh = 0; hh < 2; ++hh) {
+      const int hn0 = n0 + hh * EC;            // global column of this half
+      if (half == hh) {
 #pragma unroll
-        for (int cc = 0; cc < BN / 32; ++cc) {
-          const int cl = cc * 32 + lane, c = n0 + cl;
-          if (c >= d) break;
-          double t = ep.alpha[o] * (double)tile[rr * (BN + 1) + cl];
-#pragma unroll
-          for (int x = 0; x < kMaxAux; ++x)
-            if (x < ep.n_aux) t = fma(ep.beta[o][x], (double)ep.aux[x][(size_t)r * ep.aux_ld[x] + c], t);
-          if (r == c) t += ep.gamma[o];
-          const float v = (float)t;
-          const float hi = rna_tf32(v), lo = rna_tf32(v - hi);
-          if (ep.out_x[o]) ep.out_x[o][(size_t)r * ep.out_ld[o] + c] = v;
-          if (ep.out_hi[o]) {
-            ep.out_hi[o][(size_t)r * ep.ldp + c] = hi;
-            ep.out_lo[o][(size_t)r * ep.ldp + c] = lo;
-          }
-          vt[rr * (BN + 1) + cl] = v;
-        }
-      }
-      if (ep.out_hiT[o]) {
-        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
-        // column pass: transposed operand planes, lanes along rows of the tile
-        for (int cl = ew; cl < BN; cl += kEpiWarps) {
-          const int c = n0 + cl;
-          if (c >= d) break;
-#pragma unroll
-          for (int rc = 0; rc < BM / 32; ++rc) {
-            const int rr = rc * 32 + lane, r = m0 + rr;
-            if (r >= d) break;
-            const float v = vt[rr * (BN + 1) + cl];
-            const float hi = rna_tf32(v);
-            ep.out_hiT[o][(size_t)c * ep.ldp + r] = hi;
-            ep.out_loT[o][(size_t)c * ep.ldp + r] = rna_tf32(v - hi);
-          }
-        }
+        for (int i = 0; i < EC; ++i) tile[rl * kStageLd + i] = acc[i];
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+#ifdef NSERIES_TF32_DEBUG
+      if (warp == 4 && lane == 0 && g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 7 + hh, (unsigned long long)(clock64() - t_drained));
+#endif
+      for (int o = 0; o < ep.n_out; ++o) {
+        // fp32 combination (binary64 epilogue arithmetic measured no accuracy gain at config 3
+        // and its F2F conversions made this pass ~5x slower)
+        const float al = (float)ep.alpha[o], ga = (float)ep.gamma[o];
+        float be[kMaxAux];
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x) be[x] = (float)ep.beta[o][x];
+        float* ox = ep.out_x[o];
+        float* oh = ep.out_hi[o];
+        float* ol = ep.out_lo[o];
+        const int old_ = ep.out_ld[o];
+        // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns)
+#pragma unroll 2
+        for (int rr = ew; rr < BM; rr += kEpiWarps) {
+          const int r = m0 + rr;
+          if (r >= d) break;
+#pragma unroll
+          for (int cc = 0; cc < EC / 32; ++cc) {
+            const int cl = cc * 32 + lane, c = hn0 + cl;
+            if (c >= d) break;
+            float t = al * tile[rr * kStageLd + cl];
+#pragma unroll
+            for (int x = 0; x < kMaxAux; ++x)
+              if (x < ep.n_aux) t = fmaf(be[x], ep.aux[x][(size_t)r * ep.aux_ld[x] + c], t);
+            if (r == c) t += ga;
+            const float hi = rna_tf32(t), lo = rna_tf32(t - hi);
+            if (ox) ox[(size_t)r * old_ + c] = t;
+            if (oh) {
+              oh[(size_t)r * ep.ldp + c] = hi;
+              ol[(size_t)r * ep.ldp + c] = lo;
+            }
+            vt[rr * kStageLd + cl] = t;
+          }
+        }
+        if (ep.out_hiT[o]) {
+          asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+          // column pass: transposed operand planes, lanes along rows of the tile
+          for (int cl = ew; cl < EC; cl += kEpiWarps) {
+            const int c = hn0 + cl;
+            if (c >= d) break;
+#pragma unroll
+            for (int rc = 0; rc < BM / 32; ++rc) {
+              const int rr = rc * 32 + lane, r = m0 + rr;
+              if (r >= d) break;
+              const float v = vt[rr * kStageLd + cl];
+              const float hi = rna_tf32(v);
+              ep.out_hiT[o][(size_t)c * ep.ldp + r] = hi;
+              ep.out_loT[o][(size_t)c * ep.ldp + r] = rna_tf32(v - hi);
+            }
+          }
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+      }
     }
   }
 #ifdef NSERIES_TF32_DEBUG
@@ -435,16 +504,16 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// role 0: A operand box {32 k, 128 rows}; role 1: B operand box {32 n, 32 k}
+// role 0: A operand box {BK k, BM rows}; role 1: B operand (transposed planes) box {BK k, BN rows}
 int make_map(CUtensorMap* m, const float* base, int d, int ld, int role) {
   auto enc = get_encode();
   if (!enc) return (int)cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)d};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {32u, role == 0 ? (cuuint32_t)BM : (cuuint32_t)BK};
+  cuuint32_t box[2] = {(cuuint32_t)BK, role == 0 ? (cuuint32_t)BM : (cuuint32_t)BN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
@@ -475,8 +544,8 @@ int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const 
   CUtensorMap mxh, mxl, myh, myl;
   int rc = g_maps.get(Xh, d, ldp, 0, &mxh);
   if (!rc) rc = g_maps.get(Xl, d, ldp, 0, &mxl);
-  if (!rc) rc = g_maps.get(Yh, d, ldp, 0, &myh);   // transposed planes, same K-major box
-  if (!rc) rc = g_maps.get(Yl, d, ldp, 0, &myl);
+  if (!rc) rc = g_maps.get(Yh, d, ldp, 1, &myh);   // transposed planes, K-major box of BN rows
+  if (!rc) rc = g_maps.get(Yl, d, ldp, 1, &myl);
   if (rc) return rc;
   const size_t smem = sizeof(Smem) + 1024;
   static bool attr = false;
