@@ -29,6 +29,10 @@ struct nseries_ctx {
   std::map<std::string, Program> programs;
   nseries_stats stats{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // CUDA-graph cache: one executable graph per (program, d, dtype, buffer pointers)
+  cudaStream_t cap_stream = nullptr;
+  struct CachedGraph { cudaGraphExec_t exec; int launches; };
+  std::map<std::string, CachedGraph> graphs;
 };
 
 namespace {
@@ -296,6 +300,8 @@ nseries_status nseries_destroy(nseries_handle h) {
   if (h->stage) cudaFree(h->stage);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
   return NSERIES_OK;
 }
@@ -364,14 +370,53 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
   if (timing) cudaEventRecord(h->ev0, s);
   int launches = 0;
-  st = dt == NSERIES_F64
-           ? run_program(h, P, A, S, R_out, d, dt, s, &launches)
-           : run_program_f32(h, P, static_cast<const float*>(A), static_cast<float*>(S),
-                             static_cast<float*>(R_out), d, s, &launches);
-  if (st != NSERIES_OK) return st;
+  auto run = [&](cudaStream_t st_) {
+    return dt == NSERIES_F64
+               ? run_program(h, P, A, S, R_out, d, dt, st_, &launches)
+               : run_program_f32(h, P, static_cast<const float*>(A), static_cast<float*>(S),
+                                 static_cast<float*>(R_out), d, st_, &launches);
+  };
+  bool replayed = false;
+  if (!(flags & NSERIES_NO_GRAPH)) {
+    // The op list is replayed as one CUDA graph: the pointers are baked in, so the key holds
+    // them; capture runs on a private stream (the caller's may be the legacy NULL stream).
+    char ptrs[96];
+    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p", d, (int)dt, A, S, R_out, h->ws, h->ident);
+    const std::string gkey = key + ptrs;
+    auto git = h->graphs.find(gkey);
+    if (git == h->graphs.end()) {
+      if (h->graphs.size() >= 64) {          // bounded cache: drop everything (stream-ordered)
+        cudaStreamSynchronize(s);
+        for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
+        h->graphs.clear();
+      }
+      if (!h->cap_stream && cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cuda_fail(h, cudaGetLastError());
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      st = run(h->cap_stream);
+      e = cudaStreamEndCapture(h->cap_stream, &graph);
+      if (st != NSERIES_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      cudaGraphExec_t exec = nullptr;
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      git = h->graphs.emplace(gkey, nseries_ctx::CachedGraph{exec, launches}).first;
+    } else {
+      replayed = true;
+      launches = git->second.launches;
+    }
+    cudaError_t e = cudaGraphLaunch(git->second.exec, s);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+  } else {
+    st = run(s);
+    if (st != NSERIES_OK) return st;
+  }
   h->stats.products = P.products;
   h->stats.launches = launches;
-  h->stats.graph_replayed = 0;
+  h->stats.graph_replayed = replayed ? 1 : 0;
   h->stats.n_ops = (int)P.ops.size();
   h->stats.ms_total = 0.f;
   if (timing) {
@@ -463,7 +508,12 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
       b.out[j] = j < op.n_out ? (int8_t)slot(op.out[j]) : 0;
       b.alpha[j] = op.alpha[j];
       b.gamma[j] = op.gamma[j];
-      for (int a = 0; a < kMaxAux; ++a) b.beta[j][a] = op.beta[j][a];
+      b.falpha[j] = (float)op.alpha[j];
+      b.fgamma[j] = (float)op.gamma[j];
+      for (int a = 0; a < kMaxAux; ++a) {
+        b.beta[j][a] = op.beta[j][a];
+        b.fbeta[j][a] = (float)op.beta[j][a];
+      }
     }
   }
   h->stats = nseries_stats{};

@@ -55,61 +55,65 @@ struct Smem {
 constexpr int kThreads = 128;
 
 // ---- one fused op on shared-memory slots: out_j = alpha_j X Y + sum beta_ji aux_i + gamma_j I
+// Each warp computes a 16x16 output block (one m16 row block, two n8 blocks) so the split A
+// fragment serves two MMA triples.  Tensor-core accumulation truncates toward zero
+// (profiles/r01_tf32_accumulation_probe.txt): the hi*hi products and the two cross terms run in
+// separate accumulator chains (mode 1 there, bias halved) and are added once at the end.
 template <int DP>
 __device__ void op_f32(const BatchedOp& op, float* slots, int d) {
   using SM = Smem<float, DP>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  constexpr int MB = DP / 16, NB = DP / 8;
+  constexpr int MB = DP / 16, NP = DP / 16;     // row blocks x column-pair blocks
   const float* X = slots + op.X * SM::kSlot;
   const float* Y = slots + op.Y * SM::kSlot;
-  for (int blk = warp; blk < MB * NB; blk += kThreads / 32) {
-    const int mb = blk / NB, nb = blk % NB;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    float small[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int blk = warp; blk < MB * NP; blk += kThreads / 32) {
+    const int mb = blk / NP, np = blk % NP;
+    float big[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    float small[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     if (op.gemm) {
 #pragma unroll
       for (int kb = 0; kb < DP / 8; ++kb) {
         const int r0 = mb * 16 + g, c0 = kb * 8 + t;
-        float af[4] = {X[r0 * SM::kLd + c0], X[(r0 + 8) * SM::kLd + c0], X[r0 * SM::kLd + c0 + 4],
-                       X[(r0 + 8) * SM::kLd + c0 + 4]};
-        float bf[2] = {Y[(kb * 8 + t) * SM::kLd + nb * 8 + g], Y[(kb * 8 + t + 4) * SM::kLd + nb * 8 + g]};
-        uint32_t ah[4], al[4], bh[2], bl[2];
+        const float af[4] = {X[r0 * SM::kLd + c0], X[(r0 + 8) * SM::kLd + c0], X[r0 * SM::kLd + c0 + 4],
+                             X[(r0 + 8) * SM::kLd + c0 + 4]};
+        uint32_t ah[4], al[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) split_tf32(af[i], ah[i], al[i]);
 #pragma unroll
-        for (int i = 0; i < 2; ++i) split_tf32(bf[i], bh[i], bl[i]);
-        // Tensor-core accumulation truncates toward zero (measured: tools/tf32_acc_probe.cu,
-        // mean bias -1.4e-7 relative with a chained accumulator).  Each MMA therefore starts
-        // from zero and the k-block partials are summed with IEEE fp32 adds (bias -2.6e-8,
-        // on par with SIMT FFMA).
-        float ps[4] = {0.f, 0.f, 0.f, 0.f}, pb[4] = {0.f, 0.f, 0.f, 0.f};
-        mma_tf32(ps, al, bh);
-        mma_tf32(ps, ah, bl);
-        mma_tf32(pb, ah, bh);
+        for (int h = 0; h < 2; ++h) {
+          const int nc = (np * 2 + h) * 8 + g;
+          const float bf[2] = {Y[(kb * 8 + t) * SM::kLd + nc], Y[(kb * 8 + t + 4) * SM::kLd + nc]};
+          uint32_t bh[2], bl[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { small[i] += ps[i]; acc[i] += pb[i]; }
+          for (int i = 0; i < 2; ++i) split_tf32(bf[i], bh[i], bl[i]);
+          mma_tf32(small[h], al, bh);
+          mma_tf32(small[h], ah, bl);
+          mma_tf32(big[h], ah, bh);
+        }
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] += small[i];
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int r = mb * 16 + g + ((e & 2) ? 8 : 0), c = nb * 8 + 2 * t + (e & 1);
-      const bool inside = r < d && c < d;
-      float av[kMaxAux];
+    for (int h = 0; h < 2; ++h) {
 #pragma unroll
-      for (int x = 0; x < kMaxAux; ++x)
-        if (x < op.n_aux) av[x] = slots[op.aux[x] * SM::kSlot + r * SM::kLd + c];
-#pragma unroll
-      for (int o = 0; o < kMaxOut; ++o) {
-        if (o >= op.n_out) break;
-        float v = (float)op.alpha[o] * acc[e];
+      for (int e = 0; e < 4; ++e) {
+        const float acc = big[h][e] + small[h][e];
+        const int r = mb * 16 + g + ((e & 2) ? 8 : 0), c = (np * 2 + h) * 8 + 2 * t + (e & 1);
+        const bool inside = r < d && c < d;
+        float av[kMaxAux];
 #pragma unroll
         for (int x = 0; x < kMaxAux; ++x)
-          if (x < op.n_aux) v += (float)op.beta[o][x] * av[x];
-        if (r == c && inside) v += (float)op.gamma[o];
-        slots[op.out[o] * SM::kSlot + r * SM::kLd + c] = inside ? v : 0.f;
+          if (x < op.n_aux) av[x] = slots[op.aux[x] * SM::kSlot + r * SM::kLd + c];
+#pragma unroll
+        for (int o = 0; o < kMaxOut; ++o) {
+          if (o >= op.n_out) break;
+          float v = op.falpha[o] * acc;
+#pragma unroll
+          for (int x = 0; x < kMaxAux; ++x)
+            if (x < op.n_aux) v = fmaf(op.fbeta[o][x], av[x], v);
+          if (r == c && inside) v += op.fgamma[o];
+          slots[op.out[o] * SM::kSlot + r * SM::kLd + c] = inside ? v : 0.f;
+        }
       }
     }
   }

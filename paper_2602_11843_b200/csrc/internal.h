@@ -82,6 +82,9 @@ struct BatchedOp {
   double alpha[kMaxOut];
   double beta[kMaxOut][kMaxAux];
   double gamma[kMaxOut];
+  float falpha[kMaxOut];          // fp32 copies for the fp32 kernel (no per-element F2F)
+  float fbeta[kMaxOut][kMaxAux];
+  float fgamma[kMaxOut];
 };
 struct BatchedProgram {
   int n_ops, n_slots, a_slot, ident_slot, s_slot;
