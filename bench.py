@@ -96,31 +96,19 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+from paper_2602_11843_b200 import replicas as R  # noqa: E402  (host plumbing, no method arithmetic)
+
+
 def dist_setup(n):
-    if n <= 1 or "RANK" not in os.environ:
-        return 0, 1, 0
-    import torch
-    import torch.distributed as dist
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
-    return dist.get_rank(), dist.get_world_size(), local
+    return R.setup(n)
 
 
 def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    R.barrier(world)
 
 
 def max_over_ranks(x, world):
-    if world <= 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return R.max_over_ranks(x, world)
 
 
 # ------------------------------------------------------------------ oracle (CPU) legs
@@ -227,7 +215,7 @@ def run_native(args):
         ms, plan, st = time_plan(P, h, A, S, steps, k, args.steps, max(args.warmup, 3), flags, stream, world)
     clocks = clk.summary()
     ms_step = ms / args.steps
-    evals_per_s = world * args.steps / (ms / 1e3)
+    evals_per_s = R.aggregate_rate(args.steps, ms, world)
     tflops = plan.products * flop_per_product / (ms_step * 1e-3) / 1e12
 
     per_plan = {}
@@ -307,9 +295,7 @@ def run_native(args):
     P.nseries_destroy(h)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    R.teardown(world)
     return 0
 
 

@@ -1,0 +1,60 @@
+"""Multi-GPU plumbing for bench.py: one process per GPU, independent replicas.
+
+The single-matrix S_k(A) path is a serial chain of d x d products and does not shard
+("replicas only"): N ranks each evaluate their own replica and no data-path
+collective exists.  torch.distributed is used only for the barrier around the timed region
+and for the max-over-ranks reduction of the elapsed time; the whole-job value is
+(ranks x steps) / max elapsed.  The same helpers run on CPU with the gloo backend (tests).
+"""
+from __future__ import annotations
+
+import os
+
+
+def setup(n_requested, backend=None):
+    """Initialise the process group when launched under torchrun with n > 1.
+    Returns (rank, world, local_rank)."""
+    if n_requested <= 1 or "RANK" not in os.environ:
+        return 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group(backend)
+    return dist.get_rank(), dist.get_world_size(), local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device=None):
+    """Maximum of a host float over all ranks (elapsed times: the job is as slow as its
+    slowest replica)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    if device is None:
+        device = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(units_per_rank, elapsed_ms_max, world):
+    """Whole-job throughput: all ranks' units / the slowest rank's elapsed time."""
+    return world * units_per_rank / (elapsed_ms_max / 1e3)
+
+
+def teardown(world):
+    if world > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()

@@ -1,0 +1,53 @@
+"""world_size-2 gloo tests (CPU) of the multi-rank bench plumbing: barrier, max-over-ranks
+timing and the whole-job aggregate (replicas only, no data-path collective)."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    from paper_2602_11843_b200 import replicas as R
+    r, w, local = R.setup(world, backend="gloo")
+    R.barrier(w)
+    elapsed = 100.0 + 50.0 * r            # rank 1 is the slow replica
+    mx = R.max_over_ranks(elapsed, w, device="cpu")
+    val = R.aggregate_rate(10, mx, w)
+    q.put((r, w, mx, val))
+    R.teardown(w)
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_gloo():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=90) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    for r, w, mx, val in res:
+        assert w == 2
+        assert mx == 150.0                  # max over ranks, not the local time
+        assert abs(val - 2 * 10 / 0.150) < 1e-9
+
+
+def test_single_process_defaults():
+    from paper_2602_11843_b200 import replicas as R
+    assert R.setup(1) == (0, 1, 0)
+    assert R.max_over_ranks(3.5, 1) == 3.5
+    assert R.aggregate_rate(4, 2000.0, 1) == 2.0
