@@ -6,7 +6,7 @@
  * return S_k(A) = I + A + ... + A^{k-1}.  Cost is counted in d x d matrix
  * products.  S_k is reached by radix-kernel splitting
  * S_{mn}(A) = S_n(A) T_m(A^n) (Eq. decomposition) with
- *   - binary splitting (m=2),
+ *   - binary splitting (m=2) and ternary splitting (m=3),
  *   - the radix-5 kernel,
  *   - the exact 3-product radix-9 kernel (Theorem 1),
  *   - the approximate 4-product radix-15 kernel
@@ -46,7 +46,7 @@ typedef struct nseries_ctx* nseries_handle;
 typedef enum {
   NSERIES_OK = 0,
   NSERIES_ERR_INVALID_ARG = 1,      /* bad pointer / size / flag combination          */
-  NSERIES_ERR_UNSUPPORTED_RADIX = 2,/* radix outside {2,5,9,15} (or "+1" = 1)         */
+  NSERIES_ERR_UNSUPPORTED_RADIX = 2,/* radix outside {2,3,5,9,15} (or "+1" = 1)       */
   NSERIES_ERR_PLAN_K_MISMATCH = 3,  /* plan does not reach k (pure plan with k!=m^t) */
   NSERIES_ERR_APPROX_TELESCOPE = 4, /* approximate kernel in a telescoping-form step,
                                        or approximate radix without ALLOW_APPROX      */
@@ -66,6 +66,7 @@ typedef enum {
   NSERIES_PLAN_AUTO = 0,     /* fewest products over the radix set (default {9,5,2},
                                 {15,9,5,2} with NSERIES_ALLOW_APPROX)                 */
   NSERIES_PLAN_BINARY = 2,   /* pure plans: k must equal m^t          */
+  NSERIES_PLAN_TERNARY = 3,
   NSERIES_PLAN_RADIX5 = 5,
   NSERIES_PLAN_RADIX9 = 9,
   NSERIES_PLAN_RADIX15 = 15,
@@ -84,7 +85,7 @@ typedef enum {
 
 #define NSERIES_MAX_STEPS 128
 
-/* A plan: a sequence of steps from n = 1 to n = k.  step[i] = m in {2,5,9,15}
+/* A plan: a sequence of steps from n = 1 to n = k.  step[i] = m in {2,3,5,9,15}
  * multiplies n by m; step[i] = 1 is a "+1" step.  form[i] is filled by the
  * builder: 0 = telescoping power update R' = I - T + T R (exact kernels,
  * PAPER.md:211-212), 1 = paper residual update R' = I - M Y',
@@ -164,6 +165,28 @@ nseries_status nseries_eval_batched(nseries_handle h, const void* const* A_ptrs,
                                     int32_t d, int64_t k, const nseries_plan* plan,
                                     nseries_dtype dt, void* const* S_ptrs, uint32_t flags,
                                     void* stream);
+
+/* ---- adaptive approximate inverse -----------------------------
+ * Y ~ (I - A)^{-1} by the residual radix-kernel iteration Y_{n+1} = Y_n f(R_n),
+ * R_{n+1} = I - (I - A) Y_{n+1} with kernel m in {2,3,5,9,15}; m = 2 is
+ * Hensel lifting Y' = Y(2I - MY).  After every step the fused epilogue of
+ * the residual product accumulates ||R_n||_F^2 on the device; the host reads it (one stream
+ * synchronisation per step) and stops once ||R_n||_F / sqrt(d) <= tol (the normalised residual
+ * of App. A.3) or after max_steps.  Costs (mu_m + 2) products per step.
+ * fp64 only.  Y (and R_out if non-NULL) receive the iterate and residual of the last step. */
+typedef struct {
+  int32_t steps;        /* radix steps executed                                            */
+  int32_t products;     /* GEMMs executed                                                  */
+  int32_t converged;    /* 1 if the tolerance was reached                                  */
+  int32_t radix;
+  int64_t prefix;       /* m^steps: Y matches the Neumann series through degree prefix-1   */
+  double residual;      /* final ||I - (I - A) Y||_F / sqrt(d)                              */
+  double history[NSERIES_MAX_STEPS];  /* normalised residual after each executed step      */
+} nseries_solve_info;
+
+nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t m, double tol,
+                             int32_t max_steps, nseries_dtype dt, void* Y, void* R_out,
+                             uint32_t flags, void* stream, nseries_solve_info* info);
 
 /* Single fused-engine product C = X Y (d x d) -- the GEMM engine the plans run on, exposed
  * for accuracy micro-tests and peak measurement.  Counts as one product. */

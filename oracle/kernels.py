@@ -13,6 +13,7 @@ consumes.
 
 Circuits encoded here, each following the paper's text line by line:
   * T_2 binary:    f = 1 + z
+  * T_3 ternary:   U = B^2; T = I + B + U
   * T_5 quinary:   U = B^2; V = U(B+U); T = I+B+U+V
   * T_9 radix-9:   U = B^2; V = U(B+2U); P = 3/20 B + 2U + V;
                    Q = 11/40 B - 1/8 U + 1/4 V; W = PQ;
@@ -91,6 +92,14 @@ F = Fraction
 def circuit_binary():
     """T_2(B) = I + B, no products."""
     return [], [F(1), F(1)]
+
+
+def circuit_ternary():
+    """Ternary splitting kernel T_3 = I + B + B^2: one product.
+    basis: [I, B, U]."""
+    steps = [([0, 1], [0, 1])]                                  # U = B * B
+    final = [F(1), F(1), F(1)]
+    return steps, final
 
 
 def circuit_quinary():
@@ -191,6 +200,8 @@ def kernel_coeffs(m, variant="polished"):
     """
     if m == 2:
         steps, final = circuit_binary()
+    elif m == 3:
+        steps, final = circuit_ternary()
     elif m == 5:
         steps, final = circuit_quinary()
     elif m == 9:
@@ -203,13 +214,15 @@ def kernel_coeffs(m, variant="polished"):
     return eval_circuit(steps, final)
 
 
-MU = {2: 0, 5: 2, 9: 3, 15: 4}          # products per kernel
-EXACT = {2: True, 5: True, 9: True, 15: False}
+MU = {2: 0, 3: 1, 5: 2, 9: 3, 15: 4}    # products per kernel
+EXACT = {2: True, 3: True, 5: True, 9: True, 15: False}
 
 
 def circuit_products(m):
     if m == 2:
         return len(circuit_binary()[0])
+    if m == 3:
+        return len(circuit_ternary()[0])
     if m == 5:
         return len(circuit_quinary()[0])
     if m == 9:

@@ -15,7 +15,7 @@ STATUS_NAMES = {
     9: "NSERIES_ERR_UNSUPPORTED_SIZE",
 }
 NSERIES_F64, NSERIES_F32 = 0, 1
-NSERIES_PLAN_AUTO, NSERIES_PLAN_BINARY, NSERIES_PLAN_RADIX5 = 0, 2, 5
+NSERIES_PLAN_AUTO, NSERIES_PLAN_BINARY, NSERIES_PLAN_TERNARY, NSERIES_PLAN_RADIX5 = 0, 2, 3, 5
 NSERIES_PLAN_RADIX9, NSERIES_PLAN_RADIX15, NSERIES_PLAN_CUSTOM = 9, 15, -1
 NSERIES_ELIDE_TRIVIAL = 0x1
 NSERIES_ALLOW_APPROX = 0x2
@@ -29,7 +29,7 @@ EXPORTED = [
     "nseries_create", "nseries_destroy", "nseries_status_string", "nseries_version",
     "nseries_plan_build", "nseries_plan_finalize", "nseries_kernel_info", "nseries_eval",
     "nseries_eval_host", "nseries_eval_batched_strided", "nseries_eval_batched",
-    "nseries_matmul", "nseries_last_stats",
+    "nseries_matmul", "nseries_last_stats", "nseries_solve",
 ]
 
 
@@ -54,6 +54,12 @@ class nseries_stats(ctypes.Structure):
     _fields_ = [("products", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("graph_replayed", ctypes.c_int32), ("n_ops", ctypes.c_int32),
                 ("ms_total", ctypes.c_float)]
+
+
+class nseries_solve_info(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("products", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("radix", ctypes.c_int32), ("prefix", ctypes.c_int64), ("residual", ctypes.c_double),
+                ("history", ctypes.c_double * NSERIES_MAX_STEPS)]
 
 
 class NSeriesError(RuntimeError):
@@ -92,6 +98,8 @@ def load_library(path=None):
         "nseries_eval_batched": ([vp, vp, i32, i32, i64, plan_p, ctypes.c_int, vp, u32, vp], ctypes.c_int),
         "nseries_matmul": ([vp, ctypes.c_int, vp, vp, vp, i32, vp], ctypes.c_int),
         "nseries_last_stats": ([vp, ctypes.POINTER(nseries_stats)], ctypes.c_int),
+        "nseries_solve": ([vp, vp, i32, i32, ctypes.c_double, i32, ctypes.c_int, vp, vp, u32, vp,
+                           ctypes.POINTER(nseries_solve_info)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -226,6 +234,18 @@ def nseries_matmul(h, X, Y, C, d, dtype=None, stream=None):
     dt = _dtype_of(X) if dtype is None else dtype
     _check(load_library().nseries_matmul(h, dt, _ptr(X), _ptr(Y), _ptr(C), int(d), _stream(stream)),
            "nseries_matmul")
+
+
+def nseries_solve(h, A, d, m, tol, max_steps=NSERIES_MAX_STEPS, Y=None, R_out=None, flags=0, stream=None,
+                  dtype=None):
+    dt = _dtype_of(A) if dtype is None else dtype
+    info = nseries_solve_info()
+    _check(load_library().nseries_solve(h, _ptr(A), int(d), int(m), float(tol), int(max_steps), dt, _ptr(Y),
+                                        _ptr(R_out), int(flags), _stream(stream), ctypes.byref(info)),
+           "nseries_solve")
+    return {"steps": info.steps, "products": info.products, "converged": bool(info.converged),
+            "radix": info.radix, "prefix": info.prefix, "residual": info.residual,
+            "history": [info.history[i] for i in range(info.steps)]}
 
 
 def nseries_last_stats(h):

@@ -2,6 +2,7 @@
 // stream executor that launches one fused GEMM kernel per op.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -209,10 +210,12 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
   return NSERIES_OK;
 }
 
-// Execute a compiled program on the stream.
-nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
-                           int d, nseries_dtype dt, cudaStream_t s, int* launches) {
-  const size_t slot = (size_t)d * d * elem_size(dt);
+// Execute ops [i0, i1) of a compiled fp64 program on the stream; sumsq_op / sumsq_ptr add the
+// fused sum-of-squares reduction of output sumsq_out of op sumsq_op.
+nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
+                                 int d, cudaStream_t s, int i0, int i1, int* launches,
+                                 int sumsq_op = -1, int sumsq_out = -1, double* sumsq_ptr = nullptr) {
+  const size_t slot = (size_t)d * d * sizeof(double);
   auto ptr = [&](int v) -> void* {
     switch (P.val_kind[v]) {
       case V_USER_A: return const_cast<void*>(A);
@@ -223,30 +226,37 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
     }
   };
   int nl = 0;
-  for (const Op& op : P.ops) {
+  for (int i = i0; i < i1; ++i) {
+    const Op& op = P.ops[i];
     EpiParams ep{};
     ep.n_aux = op.n_aux;
     ep.n_out = op.n_out;
-    for (int i = 0; i < op.n_aux; ++i) ep.aux[i] = ptr(op.aux[i]);
+    for (int a = 0; a < op.n_aux; ++a) ep.aux[a] = ptr(op.aux[a]);
     for (int j = 0; j < op.n_out; ++j) {
       ep.out[j] = ptr(op.out[j]);
       ep.alpha[j] = op.alpha[j];
       ep.gamma[j] = op.gamma[j];
-      for (int i = 0; i < kMaxAux; ++i) ep.beta[j][i] = op.beta[j][i];
+      for (int a = 0; a < kMaxAux; ++a) ep.beta[j][a] = op.beta[j][a];
     }
-    int rc;
-    if (dt == NSERIES_F64) {
-      rc = op.gemm ? launch_gemm_f64(static_cast<const double*>(ptr(op.X)),
-                                     static_cast<const double*>(ptr(op.Y)), d, ep, s)
-                   : launch_axpby_f64(d, ep, s);
-    } else {
-      return NSERIES_ERR_INVALID_ARG;
+    if (i == sumsq_op) {
+      ep.sumsq = sumsq_ptr;
+      ep.sumsq_out = sumsq_out;
     }
+    const int rc = op.gemm ? launch_gemm_f64(static_cast<const double*>(ptr(op.X)),
+                                             static_cast<const double*>(ptr(op.Y)), d, ep, s)
+                           : launch_axpby_f64(d, ep, s);
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
     ++nl;
   }
   *launches = nl;
   return NSERIES_OK;
+}
+
+// Execute a compiled program on the stream.
+nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
+                           int d, nseries_dtype dt, cudaStream_t s, int* launches) {
+  if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
+  return run_program_range(h, P, A, S, R, d, s, 0, (int)P.ops.size(), launches);
 }
 
 }  // namespace
@@ -546,6 +556,99 @@ nseries_status nseries_eval_batched(nseries_handle h, const void* const* A_ptrs,
   if (batch > 0 && (!A_ptrs || !S_ptrs)) return NSERIES_ERR_INVALID_ARG;
   return eval_batched_impl(h, nullptr, 0, A_ptrs, batch, d, k, plan, dt, nullptr, 0, S_ptrs, flags,
                            stream);
+}
+
+nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t m, double tol,
+                             int32_t max_steps, nseries_dtype dt, void* Y, void* R_out,
+                             uint32_t flags, void* stream, nseries_solve_info* info) {
+  if (!h || !A || !Y || d < 1 || max_steps < 1 || max_steps > NSERIES_MAX_STEPS) return NSERIES_ERR_INVALID_ARG;
+  if (h->sticky != NSERIES_OK) return h->sticky;
+  if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
+  if (A == Y || (R_out && (A == R_out || Y == R_out))) return NSERIES_ERR_ALIAS;
+  if (kernel_mu(m) < 0) return NSERIES_ERR_UNSUPPORTED_RADIX;
+  nseries_plan p{};
+  p.n_steps = max_steps;
+  __int128 k = 1;
+  for (int i = 0; i < max_steps; ++i) {
+    if (k * m > ((__int128)1 << 62)) { p.n_steps = i; break; }   // plans reach at most 2^62
+    p.step[i] = m;
+    k *= m;
+  }
+  const uint32_t pflags = (m == 15 ? NSERIES_ALLOW_APPROX : 0u) | (flags & NSERIES_RFORM_TELESCOPE);
+  nseries_status st = finalize_plan(&p, (int64_t)k, pflags);
+  if (st != NSERIES_OK) return st;
+  Program P;
+  st = compile_plan(p, R_out != nullptr, &P);
+  if (st != NSERIES_OK) return st;
+  cudaSetDevice(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = ensure_ws(h, (size_t)P.n_slots * d * d * sizeof(double));
+  if (st != NSERIES_OK) return st;
+  if (P.needs_identity) {
+    st = ensure_identity(h, d, NSERIES_F64, s);
+    if (st != NSERIES_OK) return st;
+  }
+  double* d_ssq = nullptr;
+  if (cudaMalloc(&d_ssq, sizeof(double) * NSERIES_MAX_STEPS) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
+  cudaMemsetAsync(d_ssq, 0, sizeof(double) * NSERIES_MAX_STEPS, s);
+  nseries_solve_info inf{};
+  inf.radix = m;
+  const size_t slot = (size_t)d * d * sizeof(double);
+  auto ptr = [&](int v) -> void* {
+    switch (P.val_kind[v]) {
+      case V_USER_A: return const_cast<void*>(A);
+      case V_IDENT: return h->ident;
+      case V_USER_S: return Y;
+      case V_USER_R: return R_out;
+      default: return static_cast<char*>(h->ws) + (size_t)P.val_buf[v] * slot;
+    }
+  };
+  int op0 = 0, products = 0, launches = 0;
+  int64_t prefix = 1;
+  for (int step = 0; step < p.n_steps; ++step) {
+    int op1 = op0;
+    while (op1 < (int)P.ops.size() && P.ops[op1].step == step) ++op1;
+    // the op producing this step's residual B_n carries the fused norm
+    int rop = -1, rout = -1;
+    for (int i = op0; i < op1; ++i)
+      for (int j = 0; j < P.ops[i].n_out; ++j)
+        if (P.ops[i].out[j] == P.step_B[step]) { rop = i; rout = j; }
+    int nl = 0;
+    st = run_program_range(h, P, A, Y, R_out, d, s, op0, op1, &nl, rop, rout, d_ssq + step);
+    if (st != NSERIES_OK) { cudaFree(d_ssq); return st; }
+    for (int i = op0; i < op1; ++i) products += P.ops[i].gemm ? 1 : 0;
+    launches += nl;
+    op0 = op1;
+    prefix *= m;
+    double ssq = 0.0;
+    cudaError_t e = cudaMemcpyAsync(&ssq, d_ssq + step, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { cudaFree(d_ssq); return cuda_fail(h, e); }
+    const double res = std::sqrt(ssq) / std::sqrt((double)d);
+    inf.history[step] = res;
+    inf.steps = step + 1;
+    inf.residual = res;
+    if (res <= tol || step + 1 == p.n_steps) {
+      inf.converged = res <= tol ? 1 : 0;
+      // stopped early: the iterate / residual still live in workspace -> copy out
+      void* ys = ptr(P.step_S[step]);
+      if (ys != Y) cudaMemcpyAsync(Y, ys, slot, cudaMemcpyDeviceToDevice, s);
+      if (R_out) {
+        void* rs = ptr(P.step_B[step]);
+        if (rs != R_out) cudaMemcpyAsync(R_out, rs, slot, cudaMemcpyDeviceToDevice, s);
+      }
+      break;
+    }
+  }
+  inf.products = products;
+  inf.prefix = prefix;
+  cudaFree(d_ssq);
+  h->stats = nseries_stats{};
+  h->stats.products = products;
+  h->stats.launches = launches;
+  h->stats.n_ops = op0;
+  if (info) *info = inf;
+  return cuda_fail(h, cudaGetLastError());
 }
 
 nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X, const void* Y,

@@ -89,6 +89,7 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
   const int n = plan.n_steps;
 
   for (int i = 0; i < n; ++i) {
+    if (i > 0) { P.step_S.push_back(S); P.step_B.push_back(B); }
     const int m = plan.step[i];
     const bool first = (i == 0), last = (i + 1 == n);
     const bool skip_concat = elide && first;        // S_1 = I: concatenation is a copy
@@ -130,7 +131,11 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
     }
     int T = -1;   // kernel value T_m(B) / f(R)
     int f_for_tele = -1;
-    if (m == 5) {
+    if (m == 3) {
+      // ternary splitting: U = B^2, T_3 = I + B + U
+      Op& g1 = b.gemm(B, B, i, "x3.U");
+      T = b.out(g1, 1.0, {{B, 1.0}}, 1.0);
+    } else if (m == 5) {
       // quinary (Eqs. quinary-U/V/final 866-873)
       Op& g1 = b.gemm(B, B, i, "x5.U");
       int U = b.out(g1, 1.0, {});
@@ -195,6 +200,7 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
     B = Bn;
   }
 
+  if (n > 0) { P.step_S.push_back(S); P.step_B.push_back(B); }
   // final S -> user S; final B -> user R (optional)
   if (S == I) {   // k = 1: S = I   (degenerate, no product)
     Op& op = b.axpby(-1, "k1.identity");

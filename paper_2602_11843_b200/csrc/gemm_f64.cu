@@ -185,6 +185,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 
   // ---- fused epilogue: out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I
   const int n_aux = ep.n_aux, n_out = ep.n_out;
+  double ssq = 0.0;   // optional fused residual norm (sum of squares of out[sumsq_out])
 #pragma unroll
   for (int i = 0; i < C::kMI; ++i) {
     const int row = m0 + wm0 + i * 8 + g;
@@ -209,6 +210,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
             if (x < n_aux) { v0 += ep.beta[o][x] * av[x].x; v1 += ep.beta[o][x] * av[x].y; }
           if (row == col) v0 += ep.gamma[o];
           if (row == col + 1) v1 += ep.gamma[o];
+          if (o == ep.sumsq_out) ssq += v0 * v0 + v1 * v1;
           *reinterpret_cast<double2*>(static_cast<double*>(ep.out[o]) + off) = make_double2(v0, v1);
         }
       } else {
@@ -227,11 +229,17 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
             for (int x = 0; x < kMaxAux; ++x)
               if (x < n_aux) v += ep.beta[o][x] * av[x];
             if (row == col + e) v += ep.gamma[o];
+            if (o == ep.sumsq_out) ssq += v * v;
             static_cast<double*>(ep.out[o])[off + e] = v;
           }
         }
       }
     }
+  }
+  if (ep.sumsq) {
+#pragma unroll
+    for (int off2 = 16; off2 > 0; off2 >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, off2);
+    if ((threadIdx.x & 31) == 0 && ssq != 0.0) atomicAdd(ep.sumsq, ssq);
   }
 }
 
@@ -246,6 +254,7 @@ __global__ void axpby_f64_kernel(int d, EpiParams ep) {
       for (int x = 0; x < ep.n_aux; ++x) v += ep.beta[o][x] * static_cast<const double*>(ep.aux[x])[idx];
       if (row == col) v += ep.gamma[o];
       static_cast<double*>(ep.out[o])[idx] = v;
+      if (ep.sumsq && o == ep.sumsq_out) atomicAdd(ep.sumsq, v * v);
     }
   }
 }

@@ -59,6 +59,7 @@ struct Program {
   int final_S = -1, final_R = -1;
   bool needs_identity = false;   // the IDENT value is read from memory (paper counting)
   int products = 0;
+  std::vector<int> step_S, step_B; // value ids of (S_n, B_n) after each plan step
 };
 
 // Compile a finalized plan into an op list with workspace slot assignment.
@@ -73,6 +74,8 @@ struct EpiParams {
   double alpha[kMaxOut];
   double beta[kMaxOut][kMaxAux];
   double gamma[kMaxOut];
+  double* sumsq = nullptr;       // optional: atomically accumulate sum of squares of out[sumsq_out]
+  int sumsq_out = -1;
 };
 
 // Batched small-matrix path: the compiled op list with values mapped to shared-memory slots.

@@ -37,6 +37,7 @@ const Radix15Params& radix15_params() { return kRadix15; }
 int kernel_mu(int m) {
   switch (m) {
     case 2: return 0;   // T_2 = I + B
+    case 3: return 1;   // U = B^2, T_3 = I + B + U (ternary)
     case 5: return 2;   // U = B^2, V = U(B+U)
     case 9: return 3;   // U, V = U(B+2U), W = PQ
     case 15: return 4;  // P1..P4
@@ -44,7 +45,7 @@ int kernel_mu(int m) {
   }
 }
 
-bool kernel_exact(int m) { return m == 2 || m == 5 || m == 9; }
+bool kernel_exact(int m) { return m == 2 || m == 3 || m == 5 || m == 9; }
 
 using Poly = std::vector<double>;
 static Poly pmul(const Poly& a, const Poly& b) {
@@ -68,6 +69,7 @@ static Poly lin(const std::vector<Poly>& basis, const double* w, int n) {
 std::vector<double> kernel_poly(int m) {
   const Poly I{1.0}, B{0.0, 1.0};
   if (m == 2) return {1.0, 1.0};
+  if (m == 3) return padd(padd(I, B, 1.0), pmul(B, B), 1.0);
   if (m == 5) {
     Poly U = pmul(B, B), V = pmul(U, padd(B, U, 1.0));
     return padd(padd(padd(I, B, 1.0), U, 1.0), V, 1.0);
@@ -217,8 +219,8 @@ nseries_status build_plan(int64_t k, nseries_plan_kind kind, const int32_t* radi
   if (!out || k < 1 || k > ((int64_t)1 << 62)) return NSERIES_ERR_INVALID_ARG;
   std::memset(out, 0, sizeof(*out));
   std::vector<int> steps;
-  if (kind == NSERIES_PLAN_BINARY || kind == NSERIES_PLAN_RADIX5 || kind == NSERIES_PLAN_RADIX9 ||
-      kind == NSERIES_PLAN_RADIX15) {
+  if (kind == NSERIES_PLAN_BINARY || kind == NSERIES_PLAN_TERNARY || kind == NSERIES_PLAN_RADIX5 ||
+      kind == NSERIES_PLAN_RADIX9 || kind == NSERIES_PLAN_RADIX15) {
     int m = (int)kind;
     if (m == 15 && !(flags & NSERIES_ALLOW_APPROX)) flags |= NSERIES_ALLOW_APPROX;  // explicit request
     int64_t v = 1;

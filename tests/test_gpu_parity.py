@@ -64,7 +64,7 @@ def _run(h, A, steps, flags=0, want_R=False, dtype=torch.float64):
 
 
 PLANS = [[9, 9], [5, 5, 5], [2] * 6, [1, 2, 2], [15], [15, 15], [15, 1, 5], [9, 1, 2], [1], [2],
-         [5, 1, 9], [1, 1, 1]]
+         [5, 1, 9], [1, 1, 1], [3, 3, 3], [3, 1, 9]]
 
 
 @pytest.mark.parametrize("d", [1, 2, 3, 7, 8, 16, 31, 33, 64, 100, 130])

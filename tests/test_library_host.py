@@ -43,7 +43,7 @@ def test_version_and_status(lib):
 
 @pytest.mark.parametrize("m,k,products", [
     (5, 125, 12), (5, 625, 16), (9, 81, 10), (9, 729, 15), (15, 225, 12), (15, 3375, 18),
-    (2, 128, 14), (2, 512, 18), (2, 4096, 24), (9, 6561, 20)])
+    (2, 128, 14), (2, 512, 18), (2, 4096, 24), (9, 6561, 20), (3, 81, 12), (3, 729, 18)])
 def test_pure_plans_table2(lib, m, k, products):
     plan = P.nseries_plan_build(k, kind=m)
     assert plan.steps == [m] * len(plan.steps)
@@ -69,7 +69,7 @@ def test_approx_requires_flag(lib):
     assert e.value.status == 2
 
 
-RADIX_SETS = [[2], [5, 2], [9, 5, 2], [15, 9, 5, 2], [15, 9], [9], [5]]
+RADIX_SETS = [[2], [5, 2], [9, 5, 2], [15, 9, 5, 2], [15, 9], [9], [5], [3, 2], [9, 5, 3, 2]]
 
 
 @pytest.mark.parametrize("elide", [0, 1])
@@ -100,7 +100,7 @@ def test_forms(lib):
     assert p.forms == [2]
 
 
-@pytest.mark.parametrize("m", [2, 5, 9, 15])
+@pytest.mark.parametrize("m", [2, 3, 5, 9, 15])
 def test_kernel_info_vs_oracle(lib, m):
     info = P.nseries_kernel_info(m)
     assert info["mu"] == K.MU[m]

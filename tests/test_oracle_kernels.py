@@ -27,6 +27,11 @@ def test_binary_kernel():
     assert K.kernel_coeffs(2) == [1, 1]                                 # f = 1 + z
 
 
+def test_ternary_all_ones_exact():
+    assert K.kernel_coeffs(3) == [F(1)] * 3          # T_3 = I + B + B^2
+    assert K.circuit_products(3) == 1
+
+
 def test_quinary_all_ones_exact():
     # "Direct verification confirms T_5(B) = I + B + B^2 + B^3 + B^4"
     f = K.kernel_coeffs(5)
@@ -71,7 +76,7 @@ def test_radix9_rationals_denominators_divide_800():
 
 def test_product_counts_and_lower_bound():
     # mu_2=0, mu_5=2, mu_9=3, mu_15=4 (App. A.3 927-935)
-    for m, mu in [(2, 0), (5, 2), (9, 3), (15, 4)]:
+    for m, mu in [(2, 0), (3, 1), (5, 2), (9, 3), (15, 4)]:
         assert K.circuit_products(m) == mu == K.MU[m]
     # degree-doubling bound ceil(log2(m-1)) attained with equality
     for m in (5, 9, 15):

@@ -21,7 +21,7 @@ def test_table2_counts(m, k, binary, radix):
 
 def test_table1_coefficients():
     # coefficient C(m)/log2(m): 2.00, 1.72, 1.58, 1.54
-    printed = {2: 2.00, 5: 1.72, 9: 1.58, 15: 1.54}
+    printed = {2: 2.00, 3: 1.89, 5: 1.72, 9: 1.58, 15: 1.54}
     for m, c in printed.items():
         mu = P.MU[m]
         assert round((mu + 2) / math.log2(m), 2) == c
@@ -43,7 +43,7 @@ def test_lei_nakamura_with_plus_one():
 
 
 def test_dp_vs_bruteforce_small_k():
-    for radices in ([2], [5, 2], [9, 5, 2], RADICES, [15, 9]):
+    for radices in ([2], [5, 2], [9, 5, 2], RADICES, [15, 9], [3, 2], [9, 5, 3, 2]):
         for elide in (False, True):
             for k in range(2, 61):
                 allp = P.enumerate_plans(k, radices)
@@ -68,3 +68,9 @@ def test_elided_counts():
     assert P.plan_products([9, 9, 9], elide=True) == 13
     assert P.plan_products([9], elide=True) == 3
     assert P.plan_products([2], elide=True) == 0
+
+
+def test_ternary_counts():
+    # ternary splitting: 3 products per step, 3 log3 k; App. A.3 C(3) = 3
+    assert P.plan_products(P.pure_plan(3, 81)) == 12
+    assert P.plan_products(P.pure_plan(3, 3 ** 7)) == 21

@@ -145,7 +145,7 @@ def test_table3_normal_residuals(oracle_lib, k, printed):
 # ---------------------------------------------------------------- C-2
 
 
-@pytest.mark.parametrize("steps", [[9, 9], [5, 5, 5], [2] * 6, [5, 1, 9], [1, 2, 1, 5], [9, 1, 2]])
+@pytest.mark.parametrize("steps", [[9, 9], [5, 5, 5], [2] * 6, [5, 1, 9], [1, 2, 1, 5], [9, 1, 2], [3, 3, 3]])
 def test_plan_exact_equals_series(oracle_lib, steps):
     # exact kernels: the plan polynomial is S_k (block concatenation + telescoping)
     d = 24
