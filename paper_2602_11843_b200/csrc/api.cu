@@ -252,10 +252,45 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
   return NSERIES_OK;
 }
 
-// Execute a compiled program on the stream.
+// Execute a compiled program on the stream.  fp64 with d <= 64: the whole op list runs in one
+// single-CTA launch (plan_small.cu); otherwise one tiled GEMM launch per op.
 nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
                            int d, nseries_dtype dt, cudaStream_t s, int* launches) {
   if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
+  if (d <= 64 && (int)P.ops.size() <= kMaxSmallOps) {
+    const size_t slot = (size_t)d * d * sizeof(double);
+    auto ptr = [&](int v) -> double* {
+      switch (P.val_kind[v]) {
+        case V_USER_A: return const_cast<double*>(static_cast<const double*>(A));
+        case V_IDENT: return static_cast<double*>(h->ident);
+        case V_USER_S: return static_cast<double*>(S);
+        case V_USER_R: return static_cast<double*>(R);
+        default: return reinterpret_cast<double*>(static_cast<char*>(h->ws) + (size_t)P.val_buf[v] * slot);
+      }
+    };
+    SmallProgram sp{};
+    sp.n_ops = (int)P.ops.size();
+    for (int i = 0; i < sp.n_ops; ++i) {
+      const Op& op = P.ops[i];
+      SmallOp& so = sp.ops[i];
+      so.gemm = op.gemm ? 1 : 0;
+      so.X = op.gemm ? ptr(op.X) : nullptr;
+      so.Y = op.gemm ? ptr(op.Y) : nullptr;
+      so.n_aux = op.n_aux;
+      so.n_out = op.n_out;
+      for (int a = 0; a < op.n_aux; ++a) so.aux[a] = ptr(op.aux[a]);
+      for (int j = 0; j < op.n_out; ++j) {
+        so.out[j] = ptr(op.out[j]);
+        so.alpha[j] = op.alpha[j];
+        so.gamma[j] = op.gamma[j];
+        for (int a = 0; a < kMaxAux; ++a) so.beta[j][a] = op.beta[j][a];
+      }
+    }
+    const int rc = launch_plan_small_f64(d, sp, s);
+    if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    *launches = 1;
+    return NSERIES_OK;
+  }
   return run_program_range(h, P, A, S, R, d, s, 0, (int)P.ops.size(), launches);
 }
 

@@ -123,6 +123,24 @@ int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT
 int launch_axpby_f32(int d, const EpiParamsF32& ep, void* stream);
 inline int padded_ld(int d) { return (d + 31) / 32 * 32; }
 
+// Small single-matrix path (plan_small.cu): whole op list in one single-CTA launch, d <= 64.
+constexpr int kMaxSmallOps = 40;
+struct SmallOp {
+  const double* X;
+  const double* Y;
+  const double* aux[kMaxAux];
+  double* out[kMaxOut];
+  double alpha[kMaxOut];
+  double beta[kMaxOut][kMaxAux];
+  double gamma[kMaxOut];
+  int gemm, n_aux, n_out;
+};
+struct SmallProgram {
+  int n_ops;
+  SmallOp ops[kMaxSmallOps];
+};
+int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream);
+
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);
 int launch_axpby_f64(int d, const EpiParams& ep, void* stream);

@@ -1,0 +1,120 @@
+// plan_small.cu -- whole-plan single-CTA kernel for small single-matrix evaluations (fp64,
+// d <= 64; config 1 of BASELINE.json is d = 64).
+//
+// At d <= 64 one product is 0.26 MFLOP (~2 us on one SM), far below the launch + tail cost of
+// one grid launch per GEMM (~19 us measured per op with the tiled engine).  This kernel runs
+// the ENTIRE compiled op list in one launch on one CTA: every op stages X and Y (d x d) from L2
+// into shared memory with cp.async, 8 warps compute the d x d product on DMMA (m8n8k4 f64), and
+// the fused epilogue writes its outputs back to global memory (L2-resident at this size).  The
+// CTA barrier between ops orders the global writes of op i before the reads of op i+1.
+// Products are exactly the plan's (mu_m + 2 per step), counted per op as in the tiled path.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+
+namespace nseries {
+namespace {
+
+constexpr int kSmallThreads = 256;
+constexpr int kLd = 68;   // padded row (doubles): conflict-free 64-bit fragment loads
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp8(double* smem, const double* g, bool ok) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(ok ? 8 : 0));
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+plan_small_f64_kernel(int d, const __grid_constant__ SmallProgram prog) {
+  extern __shared__ __align__(16) double sm[];
+  double* sX = sm;
+  double* sY = sm + 64 * kLd;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  // 8 warps tile the 64 x 64 output as 4 (rows) x 2 (cols) warp tiles of 16 x 32
+  const int wm0 = (warp >> 1) * 16, wn0 = (warp & 1) * 32;
+  for (int o = 0; o < prog.n_ops; ++o) {
+    const SmallOp& op = prog.ops[o];
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (op.gemm) {
+      for (int i = tid; i < 64 * 64; i += kSmallThreads) {
+        const int r = i >> 6, c = i & 63;
+        const bool ok = r < d && c < d;
+        cp8(sX + r * kLd + c, ok ? op.X + (size_t)r * d + c : op.X, ok);
+        cp8(sY + r * kLd + c, ok ? op.Y + (size_t)r * d + c : op.Y, ok);
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      const int kmax = (d + 3) & ~3;
+      for (int k = 0; k < kmax; k += 4) {
+        double af[2], bf[4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) af[i] = sX[(wm0 + i * 8 + g) * kLd + k + t];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = sY[(k + t) * kLd + wn0 + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+      }
+    }
+    // fused epilogue (same algebra as the tiled engine)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int row = wm0 + i * 8 + g;
+      if (row >= d) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = wn0 + j * 8 + 2 * t + e;
+          if (col >= d) continue;
+          const size_t off = (size_t)row * d + col;
+          double av[kMaxAux];
+#pragma unroll
+          for (int x = 0; x < kMaxAux; ++x)
+            if (x < op.n_aux) av[x] = op.aux[x][off];
+#pragma unroll
+          for (int q = 0; q < kMaxOut; ++q) {
+            if (q >= op.n_out) break;
+            double v = op.alpha[q] * acc[i][j][e];
+#pragma unroll
+            for (int x = 0; x < kMaxAux; ++x)
+              if (x < op.n_aux) v += op.beta[q][x] * av[x];
+            if (row == col) v += op.gamma[q];
+            op.out[q][off] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();   // this op's outputs (global, L2) are visible to the next op's loads
+  }
+}
+
+}  // namespace
+
+int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream) {
+  if (d > 64 || prog.n_ops > kMaxSmallOps) return -1;
+  const size_t smem = 2 * 64 * kLd * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(plan_small_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  plan_small_f64_kernel<<<1, kSmallThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, prog);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace nseries
