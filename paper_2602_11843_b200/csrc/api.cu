@@ -525,6 +525,23 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
   }
   const Program& P = it->second;
   if ((int)P.ops.size() > kMaxBatchedOps) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  if (dt == NSERIES_F32 && d <= 32) {
+    WarpProgram wp{};
+    nseries_status wst = build_warp_program(P, &wp);
+    if (wst != NSERIES_OK) return wst;
+    h->stats = nseries_stats{};
+    h->stats.products = P.products;
+    h->stats.n_ops = wp.n_ops;
+    if (batch == 0) return NSERIES_OK;
+    if ((!A && !A_ptrs) || (!S && !S_ptrs)) return NSERIES_ERR_INVALID_ARG;
+    if (A && A == S) return NSERIES_ERR_ALIAS;
+    cudaSetDevice(h->device);
+    int rc = launch_batched_warp_f32(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, wp, stream);
+    if (rc == -1) return NSERIES_ERR_UNSUPPORTED_SIZE;
+    if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    h->stats.launches = 1;
+    return NSERIES_OK;
+  }
   BatchedProgram bp{};
   bp.n_ops = (int)P.ops.size();
   bp.a_slot = P.n_slots;

@@ -257,3 +257,59 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
 }
 
 }  // namespace nseries
+
+namespace nseries {
+
+// In-place slot assignment for executors whose ops read every operand before writing any
+// output (the warp-per-matrix batched kernel computes a whole product in registers): a value
+// whose last use is op i frees its slot BEFORE op i's outputs are placed, so an output may
+// overwrite an operand or aux it was computed from.  Only values with needs_slot[v] get a
+// slot; the others get -1.
+int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
+                         std::vector<int>* slot_of_value) {
+  const int nv = P.n_values;
+  std::vector<int> last_use(nv, -1), producer(nv, -1);
+  for (int i = 0; i < (int)P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    if (op.gemm) { last_use[op.X] = i; last_use[op.Y] = i; }
+    for (int a = 0; a < op.n_aux; ++a) last_use[op.aux[a]] = i;
+    for (int j = 0; j < op.n_out; ++j) producer[op.out[j]] = i;
+  }
+  std::vector<int>& slot = *slot_of_value;
+  slot.assign(nv, -1);
+  std::vector<int> free_slots;
+  int n_slots = 0;
+  for (int i = 0; i < (int)P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    for (int v = 0; v < nv; ++v)
+      if (last_use[v] == i && slot[v] >= 0 && producer[v] < i) free_slots.push_back(slot[v]);
+    for (int j = 0; j < op.n_out; ++j) {
+      int v = op.out[j];
+      if (!needs_slot[v]) continue;
+      int s;
+      if (!free_slots.empty()) { s = free_slots.back(); free_slots.pop_back(); }
+      else s = n_slots++;
+      slot[v] = s;
+    }
+    // outputs never read again (e.g. the final power in the paper's counting) die at once
+    for (int j = 0; j < op.n_out; ++j) {
+      int v = op.out[j];
+      if (slot[v] >= 0 && last_use[v] < 0) free_slots.push_back(slot[v]);
+    }
+  }
+  return n_slots;
+}
+
+}  // namespace nseries
+
+namespace nseries {
+std::vector<int> value_last_use(const Program& P) {
+  std::vector<int> last_use(P.n_values, -1);
+  for (int i = 0; i < (int)P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    if (op.gemm) { last_use[op.X] = i; last_use[op.Y] = i; }
+    for (int a = 0; a < op.n_aux; ++a) last_use[op.aux[a]] = i;
+  }
+  return last_use;
+}
+}  // namespace nseries

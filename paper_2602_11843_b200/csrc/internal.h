@@ -65,6 +65,12 @@ struct Program {
 // Compile a finalized plan into an op list with workspace slot assignment.
 // want_R: route the final power/residual into the user's R_out buffer.
 nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog);
+// Slot assignment allowing an op's outputs to overwrite the operands/aux that die at that op
+// (for executors that read all inputs of an op before writing; returns the slot count).
+int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
+                         std::vector<int>* slot_of_value);
+// last op index reading value v (operand or aux), -1 if never read
+std::vector<int> value_last_use(const Program& P);
 
 // ---------------------------------------------------------------- device engines
 struct EpiParams {
@@ -97,6 +103,29 @@ struct BatchedProgram {
 int launch_batched(nseries_dtype dt, const void* A, int64_t strideA, const void* const* A_ptrs,
                    void* S, int64_t strideS, void* const* S_ptrs, int batch, int d,
                    const BatchedProgram& prog, void* stream);
+
+// Warp-per-matrix batched fp32 path (batched_warp.cu, d <= 32).  Slot codes: >= 0 warp
+// shared-memory slot, kWSlotA the current A_b buffer, kWSlotI the identity (synthesised in
+// fragment registers, operands only), kWSlotNone (output not kept in shared memory).
+constexpr int kWSlotNone = -1, kWSlotA = -2, kWSlotI = -3;
+struct WarpOp {
+  int8_t gemm, X, Y, n_aux, n_out, gmask;   // gmask bit j: output j is the final S (global)
+  int8_t aux[kMaxAux], out[kMaxOut];
+  float alpha[kMaxOut];
+  float beta[kMaxOut][kMaxAux];
+  float gamma[kMaxOut];
+};
+struct WarpProgram {
+  int n_ops, n_slots;
+  unsigned probe_delay_ns;         // harness-only experiments (tools/bw_probe.cu); 0 in the library
+  WarpOp ops[kMaxBatchedOps];
+};
+// Map a compiled op list onto the warp kernel's slot codes (in-place slot assignment; the final
+// S is stored from the accumulators, and kept in a slot only if a later op reads it).
+nseries_status build_warp_program(const Program& P, WarpProgram* wp);
+int launch_batched_warp_f32(const void* A, int64_t strideA, const void* const* A_ptrs, void* S,
+                            int64_t strideS, void* const* S_ptrs, int batch, int d,
+                            const WarpProgram& prog, void* stream);
 
 // fp32 engine (gemm_tf32.cu): operands as tf32 hi/lo planes with leading dimension ldp
 // (multiple of 32): X role row-major (hi, lo), Y role transposed (hiT, loT); epilogue planes:

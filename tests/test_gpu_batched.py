@@ -114,3 +114,26 @@ def test_config4(h, steps, rows):
     errs = [O.rel_fro(S[b], _oracle(Ab[b].astype(np.float64), steps)) for b in sample]
     assert max(errs) <= TOL32, max(errs)
     assert np.all(np.isfinite(S))
+
+
+@pytest.mark.parametrize("d,pad", [(32, 0), (32, 1), (31, 3), (8, 0)])
+def test_batched_many_per_warp_strided(h, d, pad):
+    # batch >> resident warps: each warp walks many matrices (prefetch double buffer); pad > 0
+    # gives strides that break 16-byte alignment (scalar load/store paths)
+    batch = 6000
+    rng = np.random.default_rng(7 + d + pad)
+    Ab = (0.5 * rng.standard_normal((batch, d, d)) / np.sqrt(d)).astype(np.float32)
+    stride = d * d + pad
+    flat = np.zeros((batch, stride), np.float32)
+    flat[:, : d * d] = Ab.reshape(batch, -1)
+    At = torch.from_numpy(flat).cuda()
+    St = torch.full((batch, stride), float("nan"), device="cuda")
+    plan = P.nseries_plan_finalize([9, 9], 81, 0)
+    P.nseries_eval_batched_strided(h, At, stride, batch, d, 81, plan=plan, dtype=P.NSERIES_F32, S=St,
+                                   strideS=stride)
+    torch.cuda.synchronize()
+    S = St.cpu().numpy()
+    assert np.all(np.isnan(S[:, d * d:]))            # padding between matrices untouched
+    S = S[:, : d * d].reshape(batch, d, d)
+    for b in list(range(0, batch, 397)) + [batch - 1]:
+        assert O.rel_fro(S[b], _oracle(Ab[b].astype(np.float64), [9, 9])) <= TOL32, b
