@@ -41,6 +41,9 @@ namespace {
 #define NSERIES_TF32_BK 32
 #define NSERIES_TF32_STAGES 2
 #endif
+#ifndef NSERIES_TF32_RU
+#define NSERIES_TF32_RU 2   // rows per epilogue aux-load batch
+#endif
 constexpr int BM = 128, BN = NSERIES_TF32_BN, BK = NSERIES_TF32_BK, STAGES = NSERIES_TF32_STAGES;
 // BK = 16 fp32 = 64-byte rows -> SWIZZLE_64B tiles (8-row atoms of 512 B).  Each 16-wide K
 // chunk is one accumulation unit; NBUF = 4 chunk accumulators keep 4 chunks (24 MMAs) queued
@@ -374,32 +377,48 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         const float al = (float)ep.alpha[o], ga = (float)ep.gamma[o];
         float be[kMaxAux];
 #pragma unroll
-        for (int x = 0; x < kMaxAux; ++x) be[x] = (float)ep.beta[o][x];
+        for (int x = 0; x < kMaxAux; ++x) be[x] = x < ep.n_aux ? (float)ep.beta[o][x] : 0.f;
         float* ox = ep.out_x[o];
         float* oh = ep.out_hi[o];
         float* ol = ep.out_lo[o];
         const int old_ = ep.out_ld[o];
-        // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns)
-#pragma unroll 2
-        for (int rr = ew; rr < BM; rr += kEpiWarps) {
-          const int r = m0 + rr;
-          if (r >= d) break;
+        // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns).  Rows are
+        // processed in batches of RU whose aux loads are all issued before any use, so each
+        // thread keeps RU * EC/32 * n_aux global loads in flight (the pass is latency-bound).
+        constexpr int RU = NSERIES_TF32_RU;
+        const int n_aux = ep.n_aux;
+        for (int rb = ew; rb < BM; rb += kEpiWarps * RU) {
+          float av[RU][EC / 32][kMaxAux];
 #pragma unroll
-          for (int cc = 0; cc < EC / 32; ++cc) {
-            const int cl = cc * 32 + lane, c = hn0 + cl;
-            if (c >= d) break;
-            float t = al * tile[rr * kStageLd + cl];
+          for (int u = 0; u < RU; ++u)
 #pragma unroll
-            for (int x = 0; x < kMaxAux; ++x)
-              if (x < ep.n_aux) t = fmaf(be[x], ep.aux[x][(size_t)r * ep.aux_ld[x] + c], t);
-            if (r == c) t += ga;
-            const float hi = rna_tf32(t), lo = rna_tf32(t - hi);
-            if (ox) ox[(size_t)r * old_ + c] = t;
-            if (oh) {
-              oh[(size_t)r * ep.ldp + c] = hi;
-              ol[(size_t)r * ep.ldp + c] = lo;
+            for (int cc = 0; cc < EC / 32; ++cc) {
+              const int r = m0 + rb + u * kEpiWarps, c = hn0 + cc * 32 + lane;
+              const bool ok = r < d && c < d && rb + u * kEpiWarps < BM;
+#pragma unroll
+              for (int x = 0; x < kMaxAux; ++x)
+                av[u][cc][x] = (x < n_aux && ok) ? __ldg(ep.aux[x] + (size_t)r * ep.aux_ld[x] + c) : 0.f;
             }
-            vt[rr * kStageLd + cl] = t;
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {
+            const int rr = rb + u * kEpiWarps, r = m0 + rr;
+            if (rr >= BM || r >= d) break;
+#pragma unroll
+            for (int cc = 0; cc < EC / 32; ++cc) {
+              const int cl = cc * 32 + lane, c = hn0 + cl;
+              if (c >= d) break;
+              float t = al * tile[rr * kStageLd + cl];
+#pragma unroll
+              for (int x = 0; x < kMaxAux; ++x) t = fmaf(be[x], av[u][cc][x], t);   // be = 0 beyond n_aux
+              if (r == c) t += ga;
+              const float hi = rna_tf32(t), lo = rna_tf32(t - hi);
+              if (ox) ox[(size_t)r * old_ + c] = t;
+              if (oh) {
+                oh[(size_t)r * ep.ldp + c] = hi;
+                ol[(size_t)r * ep.ldp + c] = lo;
+              }
+              vt[rr * kStageLd + cl] = t;
+            }
           }
         }
         if (ep.out_hiT[o]) {
