@@ -68,13 +68,14 @@ struct Smem {
   alignas(1024) uint8_t xl[STAGES][kATileBytes];
   alignas(1024) uint8_t yh[STAGES][kBTileBytes];
   alignas(1024) uint8_t yl[STAGES][kBTileBytes];
+  uint8_t epi_extra[8192];   // the epilogue staging (3 x [128][EC+1] fp32) spills past the ring
   alignas(8) uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tmem_full[NBUF];
   uint64_t tmem_empty[NBUF];
   uint32_t tmem_base;
 };
-static_assert(2 * BM * kStageLd * 4 <= STAGES * kStageBytes, "epilogue staging must fit the TMA ring");
+static_assert(3 * BM * kStageLd * 4 <= STAGES * kStageBytes + 8192, "epilogue staging must fit the TMA ring + epi_extra");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -170,6 +171,15 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   asm volatile(
@@ -203,9 +213,141 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(r);
 }
 
+// tf32 round-to-nearest-away on the bit pattern (same result as cvt.rna.tf32.f32, incl. inf and
+// NaN; 2 instructions instead of 4)
+__device__ __forceinline__ float rna_tf32_fast(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
 #ifdef NSERIES_TF32_DEBUG
 __device__ float* g_dbg = nullptr;
 #endif
+
+// Fused epilogue of one tile (after both accumulator halves are staged in shared memory).
+// Kept out of line so that none of its state is live across the chunk-drain loop, whose
+// register budget (128-column accumulator + two in-flight TMEM loads) is the critical one.
+template <int NO>   // number of outputs (compile-time: the per-element loops fully unroll)
+__device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m0, const int n0, const int d,
+                                           const int ew, const int lane, const EpiParamsF32& ep,
+                                           const int warp, const long long t_drained) {
+  // re-derive the staging pointer from the dynamic shared array so that accesses compile to
+  // LDS / STS (a generic pointer passed in would not)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* const tiles = reinterpret_cast<float*>(smem_raw + tiles_off);
+  float* const vt = tiles + 2 * BM * kStageLd;   // output values of the current output
+  const int n_aux = ep.n_aux, ldp = ep.ldp;
+  constexpr int n_out = NO;
+  const float* auxb[kMaxAux];
+  int auxld[kMaxAux];
+#pragma unroll
+  for (int x = 0; x < kMaxAux; ++x) {
+    auxb[x] = x < n_aux ? ep.aux[x] : nullptr;
+    auxld[x] = x < n_aux ? ep.aux_ld[x] : 0;
+  }
+  for (int hh = 0; hh < 2; ++hh) {
+    const int hn0 = n0 + hh * EC;            // global column of this half
+    float* const tile = tiles + hh * BM * kStageLd;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+#ifdef NSERIES_TF32_DEBUG
+    if (warp == 4 && lane == 0 && g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 7 + hh, (unsigned long long)(clock64() - t_drained));
+#endif
+    const int ncol = min(EC, d - hn0);       // valid columns of this half (> 0 for launched tiles)
+    const int nrow = min(BM, d - m0);
+    // Pass 0 computes EVERY output from one read of the aux tiles (row-major x / hi / lo planes)
+    // and stages the first output that needs transposed planes; each further transposed output
+    // gets its own pass (staging only).  fp32 combination (binary64 epilogue arithmetic
+    // measured no accuracy gain at config 3 and its F2F conversions were ~5x slower).
+    for (int pass = 0, tnext = 0; pass < 1 + kMaxOut; ++pass) {
+      int tout = -1;                         // output staged for the column pass in this pass
+      for (int o = tnext; o < n_out; ++o)
+        if (ep.out_hiT[o]) { tout = o; break; }
+      if (pass > 0 && tout < 0) break;
+      tnext = tout + 1;
+      float al[kMaxOut], ga[kMaxOut], be[kMaxOut][kMaxAux];
+      float *ox[kMaxOut], *oh[kMaxOut], *ol[kMaxOut];
+      int old_[kMaxOut];
+#pragma unroll
+      for (int o = 0; o < kMaxOut; ++o) {
+        const bool on = o < n_out && (pass == 0 || o == tout);
+        al[o] = on ? (float)ep.alpha[o] : 0.f;
+        ga[o] = on ? (float)ep.gamma[o] : 0.f;
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x) be[o][x] = (on && x < n_aux) ? (float)ep.beta[o][x] : 0.f;
+        ox[o] = (on && pass == 0) ? ep.out_x[o] : nullptr;
+        oh[o] = (on && pass == 0) ? ep.out_hi[o] : nullptr;
+        ol[o] = (on && pass == 0) ? ep.out_lo[o] : nullptr;
+        old_[o] = o < n_out ? ep.out_ld[o] : 0;
+      }
+      // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns).  Rows are
+      // processed in batches of RU whose aux loads are all issued before any use.
+      constexpr int RU = NSERIES_TF32_RU;
+      for (int rb = ew; rb < BM; rb += kEpiWarps * RU) {
+        float av[RU][EC / 32][kMaxAux];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int rr = rb + u * kEpiWarps, r = m0 + rr;
+          const bool rok = rr < nrow;
+#pragma unroll
+          for (int x = 0; x < kMaxAux; ++x) {
+            const float* ar = auxb[x] + (size_t)r * auxld[x] + hn0;
+#pragma unroll
+            for (int cc = 0; cc < EC / 32; ++cc) {
+              const int cl = cc * 32 + lane;
+              av[u][cc][x] = (x < n_aux && rok && cl < ncol) ? __ldg(ar + cl) : 0.f;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int rr = rb + u * kEpiWarps, r = m0 + rr;
+          if (rr >= nrow) break;
+          const int dcol = r - hn0;                // tile column holding the diagonal
+#pragma unroll
+          for (int cc = 0; cc < EC / 32; ++cc) {
+            const int cl = cc * 32 + lane;
+            if (cl >= ncol) break;
+            const float a = tile[rr * kStageLd + cl];
+#pragma unroll
+            for (int o = 0; o < kMaxOut; ++o) {
+              if (o >= n_out) break;
+              float t = al[o] * a;
+#pragma unroll
+              for (int x = 0; x < kMaxAux; ++x) t = fmaf(be[o][x], av[u][cc][x], t);   // be = 0 beyond n_aux
+              if (cl == dcol) t += ga[o];
+              if (ox[o]) ox[o][(size_t)r * old_[o] + hn0 + cl] = t;
+              if (oh[o]) {
+                const float hi = rna_tf32_fast(t);
+                oh[o][(size_t)r * ldp + hn0 + cl] = hi;
+                ol[o][(size_t)r * ldp + hn0 + cl] = rna_tf32_fast(t - hi);
+              }
+              if (o == tout) vt[rr * kStageLd + cl] = t;
+            }
+          }
+        }
+      }
+      if (tout >= 0) {
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+        // column pass: transposed operand planes, lanes along rows of the tile
+        float* const ohT = ep.out_hiT[tout];
+        float* const olT = ep.out_loT[tout];
+        for (int cl = ew; cl < ncol; cl += kEpiWarps) {
+          float* const hr = ohT + (size_t)(hn0 + cl) * ldp + m0;
+          float* const lr = olT + (size_t)(hn0 + cl) * ldp + m0;
+#pragma unroll
+          for (int rc = 0; rc < BM / 32; ++rc) {
+            const int rr = rc * 32 + lane;
+            if (rr >= nrow) break;
+            const float v = vt[rr * kStageLd + cl];
+            const float hi = rna_tf32_fast(v);
+            hr[rr] = hi;
+            lr[rr] = rna_tf32_fast(v - hi);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constant__ CUtensorMap mXl,
@@ -318,6 +460,19 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       }
 #endif
     }
+  } else if (warp == 3) {
+    // ---------------- idle warp: pull this tile's aux rows into L2 while the mainloop runs, so
+    // the (latency-bound) epilogue reads hit L2
+    const int ncols = min(BN, d - n0);
+    for (int x = 0; x < ep.n_aux; ++x) {
+      const float* base = ep.aux[x];
+      const size_t ld = (size_t)ep.aux_ld[x];
+      if (((reinterpret_cast<uintptr_t>(base) | (ld * 4) | (size_t)(n0 * 4)) & 15) != 0) continue;
+      for (int rr = lane; rr < BM && m0 + rr < d; rr += 32) {
+        const float* row = base + (size_t)(m0 + rr) * ld + n0;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(row), "r"((ncols * 4) & ~15) : "memory");
+      }
+    }
   } else if (warp >= 4) {
     // ---------------- epilogue: drain chunks into fp32 registers, then the fused outputs
     const int q = warp & 3;                    // TMEM lane quarter (hardware: warp % 4)
@@ -355,92 +510,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     // ---- fused epilogue, staged through shared memory one column half at a time (the TMA
     // ring is idle: every MMA has completed and every stage was consumed).  Staging tiles
     // [128][EC+1] (acc, then the output value); the +1 pad keeps row- and column-wise
-    // accesses conflict-free.
-    float* tile = reinterpret_cast<float*>(&sm.xh[0][0]);
-    float* vt = tile + BM * kStageLd;
+    // accesses conflict-free.  All per-output parameters are hoisted into registers (the
+    // pass is instruction-bound), tf32 splits use the 2-instruction bit-pattern rna.
+    // both column halves are staged at once (the accumulator registers die here); the
+    // current output's values go to a third staging tile for the transposed column pass
+    const uint32_t tiles_off = (uint32_t)(reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw);
+    float* const tiles = reinterpret_cast<float*>(smem_raw + tiles_off);   // shared space: STS
     const int rl = q * 32 + lane;
     const int et = threadIdx.x - 128;          // 0..255 among the epilogue warps
     const int ew = et >> 5;                    // epilogue warp 0..7
-    for (int hh = 0; hh < 2; ++hh) {
-      const int hn0 = n0 + hh * EC;            // global column of this half
-      if (half == hh) {
 #pragma unroll
-        for (int i = 0; i < EC; ++i) tile[rl * kStageLd + i] = acc[i];
-      }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+    for (int i = 0; i < EC; ++i) tiles[(half * BM + rl) * kStageLd + i] = acc[i];
 #ifdef NSERIES_TF32_DEBUG
-      if (warp == 4 && lane == 0 && g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 7 + hh, (unsigned long long)(clock64() - t_drained));
+    const long long td = t_drained;
+#else
+    const long long td = 0;
 #endif
-      for (int o = 0; o < ep.n_out; ++o) {
-        // fp32 combination (binary64 epilogue arithmetic measured no accuracy gain at config 3
-        // and its F2F conversions made this pass ~5x slower)
-        const float al = (float)ep.alpha[o], ga = (float)ep.gamma[o];
-        float be[kMaxAux];
-#pragma unroll
-        for (int x = 0; x < kMaxAux; ++x) be[x] = x < ep.n_aux ? (float)ep.beta[o][x] : 0.f;
-        float* ox = ep.out_x[o];
-        float* oh = ep.out_hi[o];
-        float* ol = ep.out_lo[o];
-        const int old_ = ep.out_ld[o];
-        // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns).  Rows are
-        // processed in batches of RU whose aux loads are all issued before any use, so each
-        // thread keeps RU * EC/32 * n_aux global loads in flight (the pass is latency-bound).
-        constexpr int RU = NSERIES_TF32_RU;
-        const int n_aux = ep.n_aux;
-        for (int rb = ew; rb < BM; rb += kEpiWarps * RU) {
-          float av[RU][EC / 32][kMaxAux];
-#pragma unroll
-          for (int u = 0; u < RU; ++u)
-#pragma unroll
-            for (int cc = 0; cc < EC / 32; ++cc) {
-              const int r = m0 + rb + u * kEpiWarps, c = hn0 + cc * 32 + lane;
-              const bool ok = r < d && c < d && rb + u * kEpiWarps < BM;
-#pragma unroll
-              for (int x = 0; x < kMaxAux; ++x)
-                av[u][cc][x] = (x < n_aux && ok) ? __ldg(ep.aux[x] + (size_t)r * ep.aux_ld[x] + c) : 0.f;
-            }
-#pragma unroll
-          for (int u = 0; u < RU; ++u) {
-            const int rr = rb + u * kEpiWarps, r = m0 + rr;
-            if (rr >= BM || r >= d) break;
-#pragma unroll
-            for (int cc = 0; cc < EC / 32; ++cc) {
-              const int cl = cc * 32 + lane, c = hn0 + cl;
-              if (c >= d) break;
-              float t = al * tile[rr * kStageLd + cl];
-#pragma unroll
-              for (int x = 0; x < kMaxAux; ++x) t = fmaf(be[x], av[u][cc][x], t);   // be = 0 beyond n_aux
-              if (r == c) t += ga;
-              const float hi = rna_tf32(t), lo = rna_tf32(t - hi);
-              if (ox) ox[(size_t)r * old_ + c] = t;
-              if (oh) {
-                oh[(size_t)r * ep.ldp + c] = hi;
-                ol[(size_t)r * ep.ldp + c] = lo;
-              }
-              vt[rr * kStageLd + cl] = t;
-            }
-          }
-        }
-        if (ep.out_hiT[o]) {
-          asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
-          // column pass: transposed operand planes, lanes along rows of the tile
-          for (int cl = ew; cl < EC; cl += kEpiWarps) {
-            const int c = hn0 + cl;
-            if (c >= d) break;
-#pragma unroll
-            for (int rc = 0; rc < BM / 32; ++rc) {
-              const int rr = rc * 32 + lane, r = m0 + rr;
-              if (r >= d) break;
-              const float v = vt[rr * kStageLd + cl];
-              const float hi = rna_tf32(v);
-              ep.out_hiT[o][(size_t)c * ep.ldp + r] = hi;
-              ep.out_loT[o][(size_t)c * ep.ldp + r] = rna_tf32(v - hi);
-            }
-          }
-        }
-        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
-      }
-    }
+    if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
+    else if (ep.n_out == 2) tile_epilogue<2>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
+    else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
   }
 #ifdef NSERIES_TF32_DEBUG
   if (warp == 4 && lane == 0 && g_dbg) {
