@@ -36,6 +36,9 @@ FP64_PEAK_SOURCE = "measured: DMMA m8n8k4 register loop, tools/peak_fp64.cu (pro
 # TF32 dense peak: measured bf16 burst (MEASURED_PEAKS.json, 1631.3 TF) x the guide's nominal
 # tf32/bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md) -- "of measured x nominal ratio"
 TF32_PEAK_TFLOPS = 1631.3 * 1.1 / 2.25
+# Legacy-path (mma.sync m16n8k8 .tf32) peak used by the batched small-matrix kernel: measured
+# register loop, tools/mma_issue.cu (profiles/peaks_r01_mma_sync.txt)
+MMA_SYNC_TF32_PEAK_TFLOPS = 275.7
 REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
 
@@ -47,6 +50,7 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-plan", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 1/2/4 side lines")
     return ap.parse_args()
 
 
@@ -248,6 +252,10 @@ def run_native(args):
                                         "tf32_frac_of_peak": 3 * alg / TF32_PEAK_TFLOPS}
         del A32, S32
 
+    configs = None
+    if world == 1 and not args.no_configs:
+        configs = other_configs(P, h, stream)
+
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     A_host = A.cpu().pin_memory()
     S_host = torch.empty_like(A_host).pin_memory()
@@ -291,12 +299,70 @@ def run_native(args):
         "gpu_launches": st["launches"] * args.steps,
         "clocks": clocks,
         "per_plan": per_plan,
+        "configs": configs,
     }
     P.nseries_destroy(h)
     if rank == 0:
         print(json.dumps(line), flush=True)
     R.teardown(world)
     return 0
+
+
+def _time_evals(fn, n, n_warm, stream):
+    import torch
+    for _ in range(n_warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
+def other_configs(P, h, stream):
+    """Side measurements on BASELINE.json configs 1, 2 and 4 (device-resident inputs, CUDA events
+    on the launching stream).  Not the headline; parity for each is in tests/."""
+    import torch
+    from paper_2602_11843_b200 import inputs
+    out = {}
+    # config 1: d = 64 fp64 single matrix (latency; whole plan in one single-CTA launch)
+    A = torch.from_numpy(inputs.cfg1()).cuda()
+    S = torch.empty_like(A)
+    for name, (stp, kk) in {"x9^2": ([9, 9], 81), "x2^6": ([2] * 6, 64), "x5^3": ([5] * 3, 125)}.items():
+        plan = P.nseries_plan_finalize(stp, kk, 0)
+        ms = _time_evals(lambda: P.nseries_eval(h, A, 64, kk, plan=plan, S=S, stream=stream), 200, 20, stream)
+        out.setdefault("cfg1_d64_fp64", {})[name] = {"k": kk, "products": plan.products, "us_per_eval": ms * 1e3,
+                                                   "launches": P.nseries_last_stats(h)["launches"]}
+    # config 2: d = 1024 fp64
+    A = torch.from_numpy(inputs.cfg2()).cuda()
+    S = torch.empty_like(A)
+    for name, (stp, kk) in {"x9^3": ([9] * 3, 729), "x5^4": ([5] * 4, 625), "x2^9": ([2] * 9, 512),
+                            "x2^10": ([2] * 10, 1024)}.items():
+        plan = P.nseries_plan_finalize(stp, kk, 0)
+        ms = _time_evals(lambda: P.nseries_eval(h, A, 1024, kk, plan=plan, S=S, stream=stream), 20, 3, stream)
+        out.setdefault("cfg2_d1024_fp64", {})[name] = {
+            "k": kk, "products": plan.products, "ms_per_eval": ms,
+            "tflops": plan.products * 2.0 * 1024 ** 3 / (ms * 1e-3) / 1e12,
+            "frac_of_fp64_peak": plan.products * 2.0 * 1024 ** 3 / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS}
+    # config 4: 16384 x 32^2 fp32 batched (one launch per batch)
+    Ab = torch.from_numpy(inputs.cfg4()).cuda()
+    Sb = torch.empty_like(Ab)
+    B, d = Ab.shape[0], Ab.shape[1]
+    for name, (stp, kk) in {"x9^2": ([9, 9], 81), "x5^2": ([5, 5], 25)}.items():
+        plan = P.nseries_plan_finalize(stp, kk, 0)
+        ms = _time_evals(lambda: P.nseries_eval_batched_strided(h, Ab, d * d, B, d, kk, plan=plan, S=Sb,
+                                                                stream=stream), 20, 3, stream)
+        alg = plan.products * 2.0 * d ** 3 * B / (ms * 1e-3) / 1e12
+        out.setdefault("cfg4_batched_16384x32x32_fp32", {})[name] = {
+            "k": kk, "products_per_matrix": plan.products, "us_per_batch": ms * 1e3,
+            "matrices_per_s": B / (ms * 1e-3), "hbm_gbs": 2 * B * d * d * 4 / (ms * 1e-3) / 1e9,
+            "hbm_frac": 2 * B * d * d * 4 / (ms * 1e-3) / 1e9 / 6533.5,
+            "alg_tflops": alg, "tf32_tensor_tflops": 3 * alg,
+            "frac_of_mma_sync_tf32_peak": 3 * alg / MMA_SYNC_TF32_PEAK_TFLOPS}
+    return out
 
 
 def _traffic():
