@@ -76,7 +76,9 @@ typedef enum {
 /* flags (bitwise OR) */
 #define NSERIES_ELIDE_TRIVIAL    0x1u /* skip the S_1 = I concatenation and the unused final
                                          power/residual product; default is the
-                                         paper's counting (mu_m + 2) t of Table 2            */
+                                         paper's counting (mu_m + 2) t of Table 2.  With
+                                         R_out the final power is used, so it is computed
+                                         (one product more than plan.products_exec)      */
 #define NSERIES_ALLOW_APPROX     0x2u /* allow the approximate radix-15 kernel (residual form) */
 #define NSERIES_RFORM_TELESCOPE  0x4u /* radix-15 residual update as R' = I - f + f R instead
                                          of the paper's R' = I - M Y' (PAPER.md:557 vs 573)   */

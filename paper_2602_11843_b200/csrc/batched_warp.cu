@@ -456,7 +456,7 @@ nseries_status build_warp_program(const Program& P, WarpProgram* out) {
   const std::vector<int> last_use = value_last_use(P);
   std::vector<bool> needs(P.n_values, false);
   for (int v = 0; v < P.n_values; ++v)
-    needs[v] = P.val_kind[v] == V_TEMP || (v == P.final_S && last_use[v] >= 0);
+    needs[v] = P.val_kind[v] == V_TEMP || ((v == P.final_S || v == P.final_R) && last_use[v] >= 0);
   std::vector<int> wslot;
   WarpProgram& wp = *out;
   wp = WarpProgram{};
@@ -477,6 +477,7 @@ nseries_status build_warp_program(const Program& P, WarpProgram* out) {
     w.n_aux = (int8_t)op.n_aux;
     w.n_out = (int8_t)op.n_out;
     w.gmask = 0;
+    w.rmask = 0;
     for (int a = 0; a < kMaxAux; ++a) {
       w.aux[a] = a < op.n_aux ? (int8_t)code(op.aux[a]) : 0;
       if (a < op.n_aux && w.aux[a] == kWSlotI) return NSERIES_ERR_INVALID_ARG;   // I is gamma
@@ -484,10 +485,17 @@ nseries_status build_warp_program(const Program& P, WarpProgram* out) {
     for (int j = 0; j < kMaxOut; ++j) {
       w.out[j] = j < op.n_out ? (int8_t)code(op.out[j]) : kWSlotNone;
       if (j < op.n_out && op.out[j] == P.final_S) w.gmask |= (int8_t)(1 << j);
-      if (j < op.n_out && w.out[j] == kWSlotNone && !(w.gmask & (1 << j))) return NSERIES_ERR_INVALID_ARG;
+      if (j < op.n_out && op.out[j] == P.final_R) w.rmask |= (int8_t)(1 << j);
+      if (j < op.n_out && w.out[j] == kWSlotNone && !((w.gmask | w.rmask) & (1 << j)))
+        return NSERIES_ERR_INVALID_ARG;
       w.alpha[j] = (float)op.alpha[j];
       w.gamma[j] = (float)op.gamma[j];
-      for (int a = 0; a < kMaxAux; ++a) w.beta[j][a] = (float)op.beta[j][a];
+      w.dalpha[j] = op.alpha[j];
+      w.dgamma[j] = op.gamma[j];
+      for (int a = 0; a < kMaxAux; ++a) {
+        w.beta[j][a] = (float)op.beta[j][a];
+        w.dbeta[j][a] = op.beta[j][a];
+      }
     }
   }
   return NSERIES_OK;

@@ -93,7 +93,8 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
     const int m = plan.step[i];
     const bool first = (i == 0), last = (i + 1 == n);
     const bool skip_concat = elide && first;        // S_1 = I: concatenation is a copy
-    const bool need_power = !(elide && last);
+    // the final power is "unused" (elided) only when the caller does not ask for R_out
+    const bool need_power = !(elide && last) || want_R;
     if (m == 1) {
       // "+1": B' = B A, S' = S + B  (residual form: R' = A R, Y' = Y + R)      [reading R5]
       Op& op = b.gemm(B, A, i, "plus1");
@@ -252,7 +253,9 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
   int prods = 0;
   for (const Op& op : P.ops) prods += op.gemm ? 1 : 0;
   P.products = prods;
-  if (prods != plan.products) return NSERIES_ERR_INVALID_ARG;   // internal consistency
+  // internal consistency; an elided plan asked for R_out computes its final power (+1)
+  const int extra = (elide && want_R && n > 0 && plan.step[n - 1] != 1) ? 1 : 0;
+  if (prods != plan.products + extra) return NSERIES_ERR_INVALID_ARG;
   return NSERIES_OK;
 }
 

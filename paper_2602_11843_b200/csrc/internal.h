@@ -110,10 +110,14 @@ int launch_batched(nseries_dtype dt, const void* A, int64_t strideA, const void*
 constexpr int kWSlotNone = -1, kWSlotA = -2, kWSlotI = -3;
 struct WarpOp {
   int8_t gemm, X, Y, n_aux, n_out, gmask;   // gmask bit j: output j is the final S (global)
+  int8_t rmask;                             // rmask bit j: output j is the final R (global)
   int8_t aux[kMaxAux], out[kMaxOut];
   float alpha[kMaxOut];
   float beta[kMaxOut][kMaxAux];
   float gamma[kMaxOut];
+  double dalpha[kMaxOut];                   // binary64 copies (fp64 shared-memory plan kernel)
+  double dbeta[kMaxOut][kMaxAux];
+  double dgamma[kMaxOut];
 };
 struct WarpProgram {
   int n_ops, n_slots;
@@ -169,6 +173,9 @@ struct SmallProgram {
   SmallOp ops[kMaxSmallOps];
 };
 int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream);
+// Same, with every value of the plan resident in shared memory (slot codes of WarpProgram,
+// in-place slots); returns -1 if the plan's live set does not fit (caller falls back).
+int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
 
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);

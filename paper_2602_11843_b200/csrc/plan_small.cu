@@ -118,3 +118,126 @@ int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream) {
 }
 
 }  // namespace nseries
+
+// ---------------------------------------------------------------------------------------------
+// plan_smem_f64_kernel -- the same single-CTA whole-plan launch with EVERY value resident in
+// shared memory (d <= 64 fp64, config 1): no per-op global round trip.  Values live in 64x64
+// fp64 slots (32 KiB, unpadded, XOR-swizzled in 4-double groups: column c of row r is stored at
+// c ^ 4((r & 3) ^ 2(r & 1)), which keeps the DMMA A/B fragment loads and the epilogue's 16-byte
+// accesses bank-conflict free).  Slot assignment is in place (assign_slots_inplace): every
+// operand of an op is read before a CTA barrier, then the epilogue may overwrite values that die
+// at this op.  I as an operand (the paper's S_1 * T) is synthesised in the fragment registers;
+// the final S (and R) are written from the accumulators straight to global memory.
+namespace nseries {
+namespace {
+
+constexpr int kSlotD = 64 * 64;   // doubles per slot
+
+__device__ __forceinline__ int swz64(int r, int c) {
+  return r * 64 + (c ^ (4 * ((r & 3) ^ ((r & 1) << 1))));
+}
+
+template <bool XI, bool YI>
+__device__ __forceinline__ void smem_mma(const double* X, const double* Y, int d, int g, int t, int wm0, int wn0,
+                                         double (&acc)[2][4][2]) {
+#pragma unroll 4
+  for (int k = 0; k < 64; k += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = wm0 + i * 8 + g;
+      af[i] = XI ? ((r == k + t && r < d) ? 1.0 : 0.0) : X[swz64(r, k + t)];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = wn0 + j * 8 + g;
+      bf[j] = YI ? ((c == k + t && c < d) ? 1.0 : 0.0) : Y[swz64(k + t, c)];
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+  }
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+plan_smem_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S, double* __restrict__ R,
+                     const __grid_constant__ WarpProgram prog) {
+  extern __shared__ __align__(16) double smd[];
+  double* const sA = smd + prog.n_slots * kSlotD;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp >> 1) * 16, wn0 = (warp & 1) * 32;
+  // A -> its slot (zero padded to 64 x 64)
+  for (int i = tid; i < kSlotD; i += kSmallThreads) {
+    const int r = i >> 6, c = i & 63;
+    const bool ok = r < d && c < d;
+    cp8(sA + swz64(r, c), ok ? A + (size_t)r * d + c : A, ok);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  auto slot = [&](int code) -> double* { return code == kWSlotA ? sA : smd + (code > 0 ? code : 0) * kSlotD; };
+  for (int o = 0; o < prog.n_ops; ++o) {
+    const WarpOp& op = prog.ops[o];
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (op.gemm) {
+      if (op.X == kWSlotI) smem_mma<true, false>(nullptr, slot(op.Y), d, g, t, wm0, wn0, acc);
+      else if (op.Y == kWSlotI) smem_mma<false, true>(slot(op.X), nullptr, d, g, t, wm0, wn0, acc);
+      else smem_mma<false, false>(slot(op.X), slot(op.Y), d, g, t, wm0, wn0, acc);
+    }
+    __syncthreads();   // every operand read precedes any output write (in-place slots)
+    const double* auxp[kMaxAux];
+#pragma unroll
+    for (int x = 0; x < kMaxAux; ++x) auxp[x] = slot(x < op.n_aux ? op.aux[x] : 0);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int row = wm0 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = wn0 + j * 8 + 2 * t;
+        const int off = swz64(row, col);   // (col, col + 1) stay adjacent under the swizzle
+        double2 av[kMaxAux];
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x)
+          av[x] = x < op.n_aux ? *reinterpret_cast<const double2*>(auxp[x] + off) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < kMaxOut; ++q) {
+          if (q >= op.n_out) break;
+          double v0 = op.dalpha[q] * acc[i][j][0], v1 = op.dalpha[q] * acc[i][j][1];
+#pragma unroll
+          for (int x = 0; x < kMaxAux; ++x) {   // dbeta = 0 beyond n_aux
+            v0 = fma(op.dbeta[q][x], av[x].x, v0);
+            v1 = fma(op.dbeta[q][x], av[x].y, v1);
+          }
+          if (row == col && row < d) v0 += op.dgamma[q];
+          if (row == col + 1 && row < d) v1 += op.dgamma[q];
+          if (op.out[q] >= 0) *reinterpret_cast<double2*>(smd + op.out[q] * kSlotD + off) = make_double2(v0, v1);
+          double* gdst = (op.gmask & (1 << q)) ? S : ((op.rmask & (1 << q)) ? R : nullptr);
+          if (gdst && row < d) {
+            if (col < d) gdst[(size_t)row * d + col] = v0;
+            if (col + 1 < d) gdst[(size_t)row * d + col + 1] = v1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream) {
+  if (d > 64) return -1;
+  const size_t smem = (size_t)(prog.n_slots + 1) * kSlotD * sizeof(double);
+  if (smem > 227 * 1024) return -1;
+  cudaError_t e = cudaFuncSetAttribute(plan_smem_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  plan_smem_f64_kernel<<<1, kSmallThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, A, S, R, prog);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace nseries

@@ -59,7 +59,9 @@ def _run(h, A, steps, flags=0, want_R=False, dtype=torch.float64):
     P.nseries_eval(h, At, d, k, plan=plan, S=S, R_out=R, flags=flags)
     torch.cuda.synchronize()
     st = P.nseries_last_stats(h)
-    assert st["products"] == OP.plan_products(steps, bool(flags & P.NSERIES_ELIDE_TRIVIAL)), (steps, st)
+    elide = bool(flags & P.NSERIES_ELIDE_TRIVIAL)
+    extra = 1 if (elide and want_R and steps[-1] != 1) else 0   # R_out needs the final power
+    assert st["products"] == OP.plan_products(steps, elide) + extra, (steps, st)
     return S.cpu().numpy(), (R.cpu().numpy() if want_R else None), st
 
 
@@ -270,3 +272,34 @@ def test_config3_probes_f32(h, steps):
     S, _, _ = _run(h, A, steps, dtype=torch.float32)
     # at the fp32 tolerance the S_k oracle also bounds the radix-15 deviation (1.7e-8)
     assert _probe_parity(S.astype(np.float64), A, steps, V, 15 in steps) <= TOL32
+
+
+@pytest.fixture(scope="module")
+def h_global_small():
+    """Handle forced onto the global-slot single-CTA kernel (plan_small_f64_kernel)."""
+    import os
+    os.environ["NSERIES_NO_SMEM_SMALL"] = "1"
+    try:
+        handle = P.nseries_create(0)
+    finally:
+        del os.environ["NSERIES_NO_SMEM_SMALL"]
+    yield handle
+    P.nseries_destroy(handle)
+
+
+@pytest.mark.parametrize("d", [5, 33, 64])
+@pytest.mark.parametrize("steps,extra", [([9, 9], 0), ([9, 9], 1), ([15, 15], 0), ([15, 1, 5], 2),
+                                         ([5, 5, 5], 1), ([1, 2, 2], 0), ([1], 0), ([2], 1), ([3, 1, 9], 2)])
+@pytest.mark.parametrize("which", ["smem", "global"])
+def test_small_kernels_flags_and_R(h, h_global_small, d, steps, extra, which):
+    # both single-launch small kernels (shared-memory-resident values / global slots), with the
+    # elide / telescoping flags and the residual output R_out
+    flags = [0, P.NSERIES_ELIDE_TRIVIAL, P.NSERIES_RFORM_TELESCOPE][extra]
+    handle = h if which == "smem" else h_global_small
+    A = inputs.random_matrix(d, 11 + d, 0.7)
+    S, R, st = _run(handle, A, steps, flags=flags, want_R=True)
+    assert st["launches"] == 1
+    Sref, Rref = _oracle_full(A, steps, want_R=True)
+    assert O.rel_fro(S, Sref) <= TOL64, (d, steps, flags, which)
+    scale = float(np.sqrt(np.sum(np.asarray(Sref, dtype=LD) ** 2)))
+    assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-13
