@@ -362,6 +362,17 @@ def other_configs(P, h, stream):
             "hbm_frac": 2 * B * d * d * 4 / (ms * 1e-3) / 1e9 / 6533.5,
             "alg_tflops": alg, "tf32_tensor_tflops": 3 * alg,
             "frac_of_mma_sync_tf32_peak": 3 * alg / MMA_SYNC_TF32_PEAK_TFLOPS}
+    # config 5: d = 8192 fp64, arbitrary k = 10000 through the AUTO mixed-radix plan
+    A = inputs.cfg5(device="cuda")
+    S = torch.empty_like(A)
+    fl = P.NSERIES_ALLOW_APPROX
+    plan = P.nseries_plan_build(10000, P.NSERIES_PLAN_AUTO, [15, 9, 5, 2], fl)
+    ms = _time_evals(lambda: P.nseries_eval(h, A, 8192, 10000, plan=plan, S=S, flags=fl, stream=stream), 2, 1, stream)
+    tf = plan.products * 2.0 * 8192 ** 3 / (ms * 1e-3) / 1e12
+    out["cfg5_d8192_fp64_k10000"] = {"plan": list(plan.step[:plan.n_steps]),
+                                      "products": plan.products, "ms_per_eval": ms, "tflops": tf,
+                                      "frac_of_fp64_peak": tf / FP64_PEAK_TFLOPS}
+    del A, S
     return out
 
 

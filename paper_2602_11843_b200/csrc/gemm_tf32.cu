@@ -49,7 +49,10 @@ constexpr int BM = 128, BN = NSERIES_TF32_BN, BK = NSERIES_TF32_BK, STAGES = NSE
 // chunk is one accumulation unit; NBUF = 4 chunk accumulators keep 4 chunks (24 MMAs) queued
 // ahead of the drain round trip (commit -> epilogue tcgen05.ld -> arrive), which a 2-deep
 // buffer (128x256 tiles) could not hide (tools/tf32_timing.cu).
-constexpr int KSC = 2;                       // k-steps (of 8) per accumulation chunk (Kc = 16)
+#ifndef NSERIES_TF32_KSC
+#define NSERIES_TF32_KSC 2
+#endif
+constexpr int KSC = NSERIES_TF32_KSC;        // k-steps (of 8) per accumulation chunk (Kc = 8 KSC)
 constexpr int CPS = (BK / 8) / KSC;          // chunks per smem stage
 constexpr int NBUF = 512 / BN;               // TMEM chunk accumulators of BN columns
 constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, BN/2 columns each

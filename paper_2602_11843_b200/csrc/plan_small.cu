@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -137,39 +138,42 @@ __device__ __forceinline__ int swz64(int r, int c) {
   return r * 64 + (c ^ (4 * ((r & 3) ^ ((r & 1) << 1))));
 }
 
-template <bool XI, bool YI>
+// NW warps tile the 64 x 64 output as 4 (rows, 16 each) x NW/4 (cols, NJ n8 tiles each)
+template <int NJ, bool XI, bool YI>
 __device__ __forceinline__ void smem_mma(const double* X, const double* Y, int d, int g, int t, int wm0, int wn0,
-                                         double (&acc)[2][4][2]) {
+                                         double (&acc)[2][NJ][2]) {
 #pragma unroll 4
   for (int k = 0; k < 64; k += 4) {
-    double af[2], bf[4];
+    double af[2], bf[NJ];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int r = wm0 + i * 8 + g;
       af[i] = XI ? ((r == k + t && r < d) ? 1.0 : 0.0) : X[swz64(r, k + t)];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int c = wn0 + j * 8 + g;
       bf[j] = YI ? ((c == k + t && c < d) ? 1.0 : 0.0) : Y[swz64(k + t, c)];
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+      for (int j = 0; j < NJ; ++j) dmma884(acc[i][j], af[i], bf[j]);
   }
 }
 
-__global__ void __launch_bounds__(kSmallThreads, 1)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
 plan_smem_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S, double* __restrict__ R,
                      const __grid_constant__ WarpProgram prog) {
+  constexpr int NT = NW * 32, NJ = 8 / (NW / 4);
   extern __shared__ __align__(16) double smd[];
   double* const sA = smd + prog.n_slots * kSlotD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm0 = (warp >> 1) * 16, wn0 = (warp & 1) * 32;
+  const int wm0 = (warp & 3) * 16, wn0 = (warp >> 2) * (8 * NJ);
   // A -> its slot (zero padded to 64 x 64)
-  for (int i = tid; i < kSlotD; i += kSmallThreads) {
+  for (int i = tid; i < kSlotD; i += NT) {
     const int r = i >> 6, c = i & 63;
     const bool ok = r < d && c < d;
     cp8(sA + swz64(r, c), ok ? A + (size_t)r * d + c : A, ok);
@@ -179,15 +183,15 @@ plan_smem_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S
   auto slot = [&](int code) -> double* { return code == kWSlotA ? sA : smd + (code > 0 ? code : 0) * kSlotD; };
   for (int o = 0; o < prog.n_ops; ++o) {
     const WarpOp& op = prog.ops[o];
-    double acc[2][4][2];
+    double acc[2][NJ][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     if (op.gemm) {
-      if (op.X == kWSlotI) smem_mma<true, false>(nullptr, slot(op.Y), d, g, t, wm0, wn0, acc);
-      else if (op.Y == kWSlotI) smem_mma<false, true>(slot(op.X), nullptr, d, g, t, wm0, wn0, acc);
-      else smem_mma<false, false>(slot(op.X), slot(op.Y), d, g, t, wm0, wn0, acc);
+      if (op.X == kWSlotI) smem_mma<NJ, true, false>(nullptr, slot(op.Y), d, g, t, wm0, wn0, acc);
+      else if (op.Y == kWSlotI) smem_mma<NJ, false, true>(slot(op.X), nullptr, d, g, t, wm0, wn0, acc);
+      else smem_mma<NJ, false, false>(slot(op.X), slot(op.Y), d, g, t, wm0, wn0, acc);
     }
     __syncthreads();   // every operand read precedes any output write (in-place slots)
     const double* auxp[kMaxAux];
@@ -197,7 +201,7 @@ plan_smem_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S
     for (int i = 0; i < 2; ++i) {
       const int row = wm0 + i * 8 + g;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         const int col = wn0 + j * 8 + 2 * t;
         const int off = swz64(row, col);   // (col, col + 1) stay adjacent under the swizzle
         double2 av[kMaxAux];
@@ -234,10 +238,16 @@ int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double
   if (d > 64) return -1;
   const size_t smem = (size_t)(prog.n_slots + 1) * kSlotD * sizeof(double);
   if (smem > 227 * 1024) return -1;
-  cudaError_t e = cudaFuncSetAttribute(plan_smem_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  plan_smem_f64_kernel<<<1, kSmallThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, A, S, R, prog);
-  return (int)cudaGetLastError();
+  static const int nw = std::getenv("NSERIES_SMALL_WARPS") ? std::atoi(std::getenv("NSERIES_SMALL_WARPS")) : 16;
+  auto launch = [&](auto kern, int threads) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    kern<<<1, threads, smem, static_cast<cudaStream_t>(stream)>>>(d, A, S, R, prog);
+    return (int)cudaGetLastError();
+  };
+  if (nw == 8) return launch(plan_smem_f64_kernel<8>, 256);
+  if (nw == 32) return launch(plan_smem_f64_kernel<32>, 1024);
+  return launch(plan_smem_f64_kernel<16>, 512);
 }
 
 }  // namespace nseries
