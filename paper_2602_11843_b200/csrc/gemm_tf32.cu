@@ -38,8 +38,8 @@ namespace {
 
 #ifndef NSERIES_TF32_BN
 #define NSERIES_TF32_BN 256
-#define NSERIES_TF32_BK 32
-#define NSERIES_TF32_STAGES 2
+#define NSERIES_TF32_BK 16
+#define NSERIES_TF32_STAGES 4
 #endif
 #ifndef NSERIES_TF32_RU
 #define NSERIES_TF32_RU 2   // rows per epilogue aux-load batch
