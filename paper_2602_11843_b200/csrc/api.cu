@@ -35,7 +35,9 @@ struct nseries_ctx {
   cudaStream_t cap_stream = nullptr;
   struct CachedGraph { cudaGraphExec_t exec; int launches; };
   std::map<std::string, CachedGraph> graphs;
-  bool no_smem_small = false;   // NSERIES_NO_SMEM_SMALL=1: force the global-slot small kernel
+  // small fp64 single-matrix kernels (d <= 64): 0 cluster (default) -> 1 single-CTA shared
+  // memory -> 2 single-CTA global slots; NSERIES_SMALL_MODE selects the first one tried
+  int small_mode = 0;
 };
 
 namespace {
@@ -259,7 +261,20 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
 nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
                            int d, nseries_dtype dt, cudaStream_t s, int* launches) {
   if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
-  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && !h->no_smem_small) {
+  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode == 0) {
+    // 4-CTA cluster, each CTA a 16-row block of every value (DSMEM for the operand rows)
+    WarpProgram wp{};
+    if (build_warp_program(P, &wp, /*inplace=*/false) == NSERIES_OK) {
+      const int rc = launch_plan_cluster_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
+                                             static_cast<double*>(R), s);
+      if (rc == 0) {
+        *launches = 1;
+        return NSERIES_OK;
+      }
+      if (rc != -1) return cuda_fail(h, (cudaError_t)rc);
+    }
+  }
+  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode <= 1) {
     // whole plan with every value in shared memory (falls through if the live set is too big)
     WarpProgram wp{};
     if (build_warp_program(P, &wp) == NSERIES_OK) {
@@ -344,7 +359,7 @@ nseries_status nseries_create(nseries_handle* out, int device) {
   if (!(p.major == 10 && p.minor == 0)) return NSERIES_ERR_NO_DEVICE;   // sm_100a cubins only
   if (cudaSetDevice(device) != cudaSuccess) return NSERIES_ERR_NO_DEVICE;
   nseries_ctx* h = new nseries_ctx();
-  h->no_smem_small = std::getenv("NSERIES_NO_SMEM_SMALL") != nullptr;
+  if (const char* m = std::getenv("NSERIES_SMALL_MODE")) h->small_mode = std::atoi(m);
   h->device = device;
   cudaEventCreate(&h->ev0);
   cudaEventCreate(&h->ev1);

@@ -451,7 +451,7 @@ int launch_wpm(const void* A, int64_t strideA, const void* const* A_ptrs, void* 
 
 }  // namespace
 
-nseries_status build_warp_program(const Program& P, WarpProgram* out) {
+nseries_status build_warp_program(const Program& P, WarpProgram* out, bool inplace) {
   if ((int)P.ops.size() > kMaxBatchedOps) return NSERIES_ERR_UNSUPPORTED_SIZE;
   const std::vector<int> last_use = value_last_use(P);
   std::vector<bool> needs(P.n_values, false);
@@ -460,7 +460,7 @@ nseries_status build_warp_program(const Program& P, WarpProgram* out) {
   std::vector<int> wslot;
   WarpProgram& wp = *out;
   wp = WarpProgram{};
-  wp.n_slots = assign_slots_inplace(P, needs, &wslot);
+  wp.n_slots = assign_slots_inplace(P, needs, &wslot, inplace);
   wp.n_ops = (int)P.ops.size();
   auto code = [&](int v) -> int {
     if (P.val_kind[v] == V_USER_A) return kWSlotA;

@@ -263,13 +263,15 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
 
 namespace nseries {
 
-// In-place slot assignment for executors whose ops read every operand before writing any
-// output (the warp-per-matrix batched kernel computes a whole product in registers): a value
-// whose last use is op i frees its slot BEFORE op i's outputs are placed, so an output may
-// overwrite an operand or aux it was computed from.  Only values with needs_slot[v] get a
-// slot; the others get -1.
+// Slot assignment for the shared-memory executors.  inplace = true: for executors whose ops read
+// every operand before writing any output (the warp-per-matrix batched kernel computes a whole
+// product in registers): a value whose last use is op i frees its slot BEFORE op i's outputs
+// are placed, so an output may overwrite an operand or aux it was computed from.  inplace =
+// false: outputs never share a slot with a value read by the same op (the cluster kernel, whose
+// CTAs read each other's operand rows while writing their own outputs).  Only values with
+// needs_slot[v] get a slot; the others get -1.
 int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
-                         std::vector<int>* slot_of_value) {
+                         std::vector<int>* slot_of_value, bool inplace) {
   const int nv = P.n_values;
   std::vector<int> last_use(nv, -1), producer(nv, -1);
   for (int i = 0; i < (int)P.ops.size(); ++i) {
@@ -284,8 +286,9 @@ int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
   int n_slots = 0;
   for (int i = 0; i < (int)P.ops.size(); ++i) {
     const Op& op = P.ops[i];
-    for (int v = 0; v < nv; ++v)
-      if (last_use[v] == i && slot[v] >= 0 && producer[v] < i) free_slots.push_back(slot[v]);
+    if (inplace)
+      for (int v = 0; v < nv; ++v)
+        if (last_use[v] == i && slot[v] >= 0 && producer[v] < i) free_slots.push_back(slot[v]);
     for (int j = 0; j < op.n_out; ++j) {
       int v = op.out[j];
       if (!needs_slot[v]) continue;
@@ -294,6 +297,9 @@ int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
       else s = n_slots++;
       slot[v] = s;
     }
+    if (!inplace)   // operands / aux dying here are freed only after the outputs are placed
+      for (int v = 0; v < nv; ++v)
+        if (last_use[v] == i && slot[v] >= 0 && producer[v] < i) free_slots.push_back(slot[v]);
     // outputs never read again (e.g. the final power in the paper's counting) die at once
     for (int j = 0; j < op.n_out; ++j) {
       int v = op.out[j];

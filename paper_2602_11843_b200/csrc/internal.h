@@ -68,7 +68,7 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
 // Slot assignment allowing an op's outputs to overwrite the operands/aux that die at that op
 // (for executors that read all inputs of an op before writing; returns the slot count).
 int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
-                         std::vector<int>* slot_of_value);
+                         std::vector<int>* slot_of_value, bool inplace = true);
 // last op index reading value v (operand or aux), -1 if never read
 std::vector<int> value_last_use(const Program& P);
 
@@ -126,7 +126,7 @@ struct WarpProgram {
 };
 // Map a compiled op list onto the warp kernel's slot codes (in-place slot assignment; the final
 // S is stored from the accumulators, and kept in a slot only if a later op reads it).
-nseries_status build_warp_program(const Program& P, WarpProgram* wp);
+nseries_status build_warp_program(const Program& P, WarpProgram* wp, bool inplace = true);
 int launch_batched_warp_f32(const void* A, int64_t strideA, const void* const* A_ptrs, void* S,
                             int64_t strideS, void* const* S_ptrs, int batch, int d,
                             const WarpProgram& prog, void* stream);
@@ -176,6 +176,9 @@ int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream);
 // Same, with every value of the plan resident in shared memory (slot codes of WarpProgram,
 // in-place slots); returns -1 if the plan's live set does not fit (caller falls back).
 int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
+// Cluster of 4 CTAs, each holding a 16-row block of every value (operand rows of the other CTAs
+// read through distributed shared memory); prog built with inplace = false.  -1 if unsupported.
+int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
 
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);

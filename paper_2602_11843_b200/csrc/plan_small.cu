@@ -251,3 +251,176 @@ int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double
 }
 
 }  // namespace nseries
+
+// ---------------------------------------------------------------------------------------------
+// plan_cluster_f64_kernel -- d <= 64 fp64 single matrix on a CLUSTER of 4 CTAs (4 SMs).  CTA c
+// owns rows [16c, 16c+16) of every value (its slots hold only that row block, swizzled as
+// above).  A product out = X Y needs X's local rows and ALL rows of Y: the 48 remote rows are
+// read through distributed shared memory (ld from the peer CTA's slot, mapa-mapped pointers).
+// The epilogue writes only local rows (plus this CTA's rows of the final S / R to HBM), and a
+// cluster barrier after every op makes them visible to the peers' next reads.  Slots are
+// assigned without in-place reuse (a peer may still be reading an operand row while this CTA
+// writes its outputs), so one barrier per op suffices.
+#include <cooperative_groups.h>
+namespace nseries {
+namespace {
+
+constexpr int kClusterCtas = 4, kRowsPerCta = 64 / kClusterCtas;     // 16
+#ifdef NSERIES_SMALL_PROFILE
+__device__ long long g_small_prof[256];
+#endif
+constexpr int kCSlotD = kRowsPerCta * 64;                               // doubles per slot block
+
+// op decoded once per CTA into shared memory (resolved slot offsets; LDS instead of indexed
+// constant-bank loads on the per-op critical path)
+struct __align__(16) ClusterOp {
+  double alpha[kMaxOut], beta[kMaxOut][kMaxAux], gamma[kMaxOut];
+  int x, y, kind, n_aux, n_out, gmask, rmask, pad;   // kind: 0 axpby, 1 gemm, 2 X = I, 3 Y = I
+  int aux[kMaxAux], out[kMaxOut];                      // offsets (doubles); out < 0: not kept
+};
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(256, 1)
+plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S, double* __restrict__ R,
+                        const __grid_constant__ WarpProgram prog) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double smc[];
+  const int rank = (int)cluster.block_rank();
+  const int r0 = rank * kRowsPerCta;
+  const int n_ops = prog.n_ops;
+  double* const sA = smc + prog.n_slots * kCSlotD;
+  ClusterOp* const sops = reinterpret_cast<ClusterOp*>(smc + (prog.n_slots + 1) * kCSlotD);
+  const double* peer[kClusterCtas];
+#pragma unroll
+  for (int c = 0; c < kClusterCtas; ++c) peer[c] = cluster.map_shared_rank(smc, c);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wn0 = warp * 8;            // 8 warps x 8 output columns; each warp all 16 local rows
+  auto off_of = [&](int code) -> int { return code == kWSlotA ? prog.n_slots * kCSlotD : (code > 0 ? code : 0) * kCSlotD; };
+  for (int i = tid; i < n_ops; i += 256) {
+    const WarpOp& w = prog.ops[i];
+    ClusterOp c;
+    c.kind = !w.gemm ? 0 : (w.X == kWSlotI ? 2 : (w.Y == kWSlotI ? 3 : 1));
+    c.x = off_of(w.X);
+    c.y = off_of(w.Y);
+    c.n_aux = w.n_aux;
+    c.n_out = w.n_out;
+    c.gmask = w.gmask;
+    c.rmask = w.rmask;
+    c.pad = 0;
+    for (int x = 0; x < kMaxAux; ++x) c.aux[x] = off_of(x < w.n_aux ? w.aux[x] : 0);
+    for (int q = 0; q < kMaxOut; ++q) {
+      c.out[q] = (q < w.n_out && w.out[q] >= 0) ? w.out[q] * kCSlotD : -1;
+      c.alpha[q] = w.dalpha[q];
+      c.gamma[q] = w.dgamma[q];
+      for (int x = 0; x < kMaxAux; ++x) c.beta[q][x] = w.dbeta[q][x];
+    }
+    sops[i] = c;
+  }
+  // local row block of A (zero padded)
+  for (int i = tid; i < kCSlotD; i += 256) {
+    const int rl = i >> 6, c = i & 63, r = r0 + rl;
+    const bool ok = r < d && c < d;
+    cp8(sA + swz64(rl, c), ok ? A + (size_t)r * d + c : A, ok);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  cluster.sync();
+#ifdef NSERIES_SMALL_PROFILE
+  long long tp0 = clock64();
+  if (tid == 0 && rank == 0) g_small_prof[0] = tp0;
+#endif
+  for (int o = 0; o < n_ops; ++o) {
+    const ClusterOp& op = sops[o];
+    // KS independent partial accumulators per row block (k-steps s with s % KS == p) keep KS
+    // DMMA chains in flight per row block instead of one 16-long dependent chain
+    constexpr int KS = 4;
+    double part[2][KS][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int p = 0; p < KS; ++p) part[i][p][0] = part[i][p][1] = 0.0;
+    const int kind = op.kind;
+    if (kind != 0) {
+      const bool xi = kind == 2, yi = kind == 3;
+      const int xo = op.x, yo = op.y;
+      // B fragments: Y[k + t][wn0 + g] for the 16 k-steps, rows owned by CTA (k + t) / 16;
+      // all issued before the first MMA (remote latency)
+      double bf[16];
+      const int col = wn0 + g;
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const int k = 4 * s + t;
+        bf[s] = yi ? ((k == col && col < d) ? 1.0 : 0.0) : peer[k >> 4][yo + swz64(k & 15, col)];
+      }
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const int k = 4 * s + t;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int rl = i * 8 + g;
+          const double a = xi ? ((r0 + rl == k && r0 + rl < d) ? 1.0 : 0.0) : smc[xo + swz64(rl, k)];
+          dmma884(part[i][s % KS], a, bf[s]);
+        }
+      }
+    }
+    double acc[2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) acc[i][e] = (part[i][0][e] + part[i][1][e]) + (part[i][2][e] + part[i][3][e]);
+#ifdef NSERIES_SMALL_PROFILE
+    if (tid == 0 && rank == 0) g_small_prof[1 + 3 * o] = clock64() + (long long)(acc[0][0] * 0.0);
+#endif
+    // epilogue on local rows (no barrier needed before it: outputs never alias this op's operands)
+    const int n_aux = op.n_aux, n_out = op.n_out;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int rl = i * 8 + g, row = r0 + rl;
+      const int colp = wn0 + 2 * t;
+      const int off = swz64(rl, colp);
+      double2 av[kMaxAux];
+#pragma unroll
+      for (int x = 0; x < kMaxAux; ++x)
+        av[x] = x < n_aux ? *reinterpret_cast<const double2*>(smc + op.aux[x] + off) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kMaxOut; ++q) {
+        if (q >= n_out) break;
+        double v0 = op.alpha[q] * acc[i][0], v1 = op.alpha[q] * acc[i][1];
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x) {
+          v0 = fma(op.beta[q][x], av[x].x, v0);
+          v1 = fma(op.beta[q][x], av[x].y, v1);
+        }
+        if (row == colp && row < d) v0 += op.gamma[q];
+        if (row == colp + 1 && row < d) v1 += op.gamma[q];
+        if (op.out[q] >= 0) *reinterpret_cast<double2*>(smc + op.out[q] + off) = make_double2(v0, v1);
+        double* gdst = (op.gmask & (1 << q)) ? S : ((op.rmask & (1 << q)) ? R : nullptr);
+        if (gdst && row < d) {
+          if (colp < d) gdst[(size_t)row * d + colp] = v0;
+          if (colp + 1 < d) gdst[(size_t)row * d + colp + 1] = v1;
+        }
+      }
+    }
+#ifdef NSERIES_SMALL_PROFILE
+    if (tid == 0 && rank == 0) g_small_prof[2 + 3 * o] = clock64();
+#endif
+    cluster.sync();   // this op's rows are visible to every CTA before the next op reads them
+#ifdef NSERIES_SMALL_PROFILE
+    if (tid == 0 && rank == 0) g_small_prof[3 + 3 * o] = clock64();
+#endif
+  }
+}
+
+}  // namespace
+
+int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream) {
+  if (d > 64) return -1;
+  const size_t smem = (size_t)(prog.n_slots + 1) * kCSlotD * sizeof(double) + (size_t)prog.n_ops * sizeof(ClusterOp);
+  if (smem > 227 * 1024) return -1;
+  cudaError_t e = cudaFuncSetAttribute(plan_cluster_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  plan_cluster_f64_kernel<<<kClusterCtas, 256, smem, static_cast<cudaStream_t>(stream)>>>(d, A, S, R, prog);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace nseries

@@ -274,28 +274,34 @@ def test_config3_probes_f32(h, steps):
     assert _probe_parity(S.astype(np.float64), A, steps, V, 15 in steps) <= TOL32
 
 
-@pytest.fixture(scope="module")
-def h_global_small():
-    """Handle forced onto the global-slot single-CTA kernel (plan_small_f64_kernel)."""
+def _handle_with_small_mode(mode):
     import os
-    os.environ["NSERIES_NO_SMEM_SMALL"] = "1"
+    os.environ["NSERIES_SMALL_MODE"] = str(mode)
     try:
-        handle = P.nseries_create(0)
+        return P.nseries_create(0)
     finally:
-        del os.environ["NSERIES_NO_SMEM_SMALL"]
-    yield handle
-    P.nseries_destroy(handle)
+        del os.environ["NSERIES_SMALL_MODE"]
+
+
+@pytest.fixture(scope="module")
+def h_small_modes():
+    """Handles forced onto each single-launch small kernel: 0 = 4-CTA cluster (default),
+    1 = single-CTA shared-memory values, 2 = single-CTA global slots."""
+    hs = {m: _handle_with_small_mode(m) for m in (0, 1, 2)}
+    yield hs
+    for x in hs.values():
+        P.nseries_destroy(x)
 
 
 @pytest.mark.parametrize("d", [5, 33, 64])
 @pytest.mark.parametrize("steps,extra", [([9, 9], 0), ([9, 9], 1), ([15, 15], 0), ([15, 1, 5], 2),
                                          ([5, 5, 5], 1), ([1, 2, 2], 0), ([1], 0), ([2], 1), ([3, 1, 9], 2)])
-@pytest.mark.parametrize("which", ["smem", "global"])
-def test_small_kernels_flags_and_R(h, h_global_small, d, steps, extra, which):
-    # both single-launch small kernels (shared-memory-resident values / global slots), with the
-    # elide / telescoping flags and the residual output R_out
+@pytest.mark.parametrize("which", [0, 1, 2])
+def test_small_kernels_flags_and_R(h_small_modes, d, steps, extra, which):
+    # the three single-launch small kernels (cluster / shared-memory values / global slots), with
+    # the elide / telescoping flags and the residual output R_out
     flags = [0, P.NSERIES_ELIDE_TRIVIAL, P.NSERIES_RFORM_TELESCOPE][extra]
-    handle = h if which == "smem" else h_global_small
+    handle = h_small_modes[which]
     A = inputs.random_matrix(d, 11 + d, 0.7)
     S, R, st = _run(handle, A, steps, flags=flags, want_R=True)
     assert st["launches"] == 1
