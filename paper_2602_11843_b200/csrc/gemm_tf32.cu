@@ -58,6 +58,7 @@ constexpr int NBUF = 512 / BN;               // TMEM chunk accumulators of BN co
 constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, BN/2 columns each
 constexpr int EC = BN / 2;                   // columns per epilogue thread
 constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kFinalWarps = kThreads / 32;    // every warp runs the final epilogue passes
 constexpr uint32_t kATileBytes = BM * BK * 4;   // 8 KB  (128 rows x 16 k)
 constexpr uint32_t kBTileBytes = BN * BK * 4;   // 8 KB (128 rows of Y^T x 16 k)
 constexpr uint32_t kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
@@ -250,7 +251,7 @@ __device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m
   for (int hh = 0; hh < 2; ++hh) {
     const int hn0 = n0 + hh * EC;            // global column of this half
     float* const tile = tiles + hh * BM * kStageLd;
-    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
 #ifdef NSERIES_TF32_DEBUG
     if (warp == 4 && lane == 0 && g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 7 + hh, (unsigned long long)(clock64() - t_drained));
 #endif
@@ -284,11 +285,11 @@ __device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m
       // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns).  Rows are
       // processed in batches of RU whose aux loads are all issued before any use.
       constexpr int RU = NSERIES_TF32_RU;
-      for (int rb = ew; rb < BM; rb += kEpiWarps * RU) {
+      for (int rb = ew; rb < BM; rb += kFinalWarps * RU) {
         float av[RU][EC / 32][kMaxAux];
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
-          const int rr = rb + u * kEpiWarps, r = m0 + rr;
+          const int rr = rb + u * kFinalWarps, r = m0 + rr;
           const bool rok = rr < nrow;
 #pragma unroll
           for (int x = 0; x < kMaxAux; ++x) {
@@ -302,7 +303,7 @@ __device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m
         }
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
-          const int rr = rb + u * kEpiWarps, r = m0 + rr;
+          const int rr = rb + u * kFinalWarps, r = m0 + rr;
           if (rr >= nrow) break;
           const int dcol = r - hn0;                // tile column holding the diagonal
 #pragma unroll
@@ -329,11 +330,11 @@ __device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m
         }
       }
       if (tout >= 0) {
-        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
         // column pass: transposed operand planes, lanes along rows of the tile
         float* const ohT = ep.out_hiT[tout];
         float* const olT = ep.out_loT[tout];
-        for (int cl = ew; cl < ncol; cl += kEpiWarps) {
+        for (int cl = ew; cl < ncol; cl += kFinalWarps) {
           float* const hr = ohT + (size_t)(hn0 + cl) * ldp + m0;
           float* const lr = olT + (size_t)(hn0 + cl) * ldp + m0;
 #pragma unroll
@@ -347,7 +348,7 @@ __device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m
           }
         }
       }
-      asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps));
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
     }
   }
 }
@@ -517,18 +518,21 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     // pass is instruction-bound), tf32 splits use the 2-instruction bit-pattern rna.
     // both column halves are staged at once (the accumulator registers die here); the
     // current output's values go to a third staging tile for the transposed column pass
-    const uint32_t tiles_off = (uint32_t)(reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw);
-    float* const tiles = reinterpret_cast<float*>(smem_raw + tiles_off);   // shared space: STS
+    float* const tiles = reinterpret_cast<float*>(smem_raw + (reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw));
     const int rl = q * 32 + lane;
-    const int et = threadIdx.x - 128;          // 0..255 among the epilogue warps
-    const int ew = et >> 5;                    // epilogue warp 0..7
 #pragma unroll
     for (int i = 0; i < EC; ++i) tiles[(half * BM + rl) * kStageLd + i] = acc[i];
+  }
+  {
+    // ---- final epilogue passes on ALL warps (the producer / MMA / allocator / prefetch warps
+    // are idle by now); the first barrier inside orders the staging above
 #ifdef NSERIES_TF32_DEBUG
     const long long td = t_drained;
 #else
     const long long td = 0;
 #endif
+    const uint32_t tiles_off = (uint32_t)(reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw);
+    const int ew = warp >= 4 ? warp - 4 : warp + kEpiWarps;   // 0..11
     if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
     else if (ep.n_out == 2) tile_epilogue<2>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
     else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
