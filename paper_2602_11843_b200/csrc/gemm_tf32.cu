@@ -228,10 +228,11 @@ __device__ float* g_dbg = nullptr;
 #endif
 
 // Fused epilogue of one tile (after both accumulator halves are staged in shared memory).
-// Kept out of line so that none of its state is live across the chunk-drain loop, whose
-// register budget (128-column accumulator + two in-flight TMEM loads) is the critical one.
+// Inlined: an out-of-line version reads the __grid_constant__ parameters through generic loads
+// (~10 K cycles per pass); the drain loop stays spill-free as long as the staging pointer is
+// derived without an integer round trip through the shared-window address.
 template <int NO>   // number of outputs (compile-time: the per-element loops fully unroll)
-__device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m0, const int n0, const int d,
+__device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const int m0, const int n0, const int d,
                                            const int ew, const int lane, const EpiParamsF32& ep,
                                            const int warp, const long long t_drained) {
   // re-derive the staging pointer from the dynamic shared array so that accesses compile to
@@ -329,6 +330,10 @@ __device__ __noinline__ void tile_epilogue(const uint32_t tiles_off, const int m
           }
         }
       }
+#ifdef NSERIES_TF32_DEBUG
+      if (warp == 4 && lane == 0 && g_dbg && hh == 0 && pass == 0)
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 9, (unsigned long long)(clock64() - t_drained));
+#endif
       if (tout >= 0) {
         asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
         // column pass: transposed operand planes, lanes along rows of the tile

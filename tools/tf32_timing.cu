@@ -9,11 +9,13 @@ int main() {
   cudaMalloc(&Xh, n*4); cudaMalloc(&Xl, n*4); cudaMalloc(&Yh, n*4); cudaMalloc(&Yl, n*4); cudaMalloc(&C, n*4);
   for (int i = 0; i < 6; ++i) { cudaMalloc(&P[i], n * 4); cudaMemset(P[i], 0, n * 4); }
   cudaMemset(Xh, 0, n*4); cudaMemset(Xl, 0, n*4); cudaMemset(Yh, 0, n*4); cudaMemset(Yl, 0, n*4);
-  unsigned long long* dbg; cudaMalloc(&dbg, 128); cudaMemset(dbg, 0, 128);
+  unsigned long long* dbg; cudaMalloc(&dbg, 256); cudaMemset(dbg, 0, 256);
   float* dp = (float*)dbg; cudaMemcpyToSymbol(g_dbg, &dp, sizeof(dp));
-  for (int variant = 0; variant < 2; ++variant) {
+  for (int variant = 0; variant < 4; ++variant) {
     EpiParamsF32 ep{}; ep.ldp = ldp;
     if (variant == 0) { ep.n_out = 1; ep.out_x[0] = C; ep.out_ld[0] = d; ep.alpha[0] = 1.0; }
+    else if (variant == 2) { ep.n_out = 1; ep.out_ld[0] = d; ep.alpha[0] = 1.0; }   // no stores at all
+    else if (variant == 3) { ep.n_out = 1; ep.out_hiT[0] = P[2]; ep.out_loT[0] = P[3]; ep.out_ld[0] = d; ep.alpha[0] = 1.0; }
     else {
       ep.n_out = 3; ep.n_aux = 1; ep.aux[0] = P[5]; ep.aux_ld[0] = d;
       ep.out_x[0] = C; ep.out_ld[0] = d; ep.alpha[0] = 1.0;
@@ -21,7 +23,7 @@ int main() {
       ep.out_hiT[2] = P[2]; ep.out_loT[2] = P[3]; ep.out_ld[2] = d; ep.alpha[2] = 0.3; ep.beta[2][0] = 0.1; ep.gamma[2] = 1;
     }
     launch_gemm_tf32x3(Xh, Xl, Yh, Yl, d, ldp, ep, 0); cudaDeviceSynchronize();
-    cudaMemset(dbg, 0, 128);
+    cudaMemset(dbg, 0, 256);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0); launch_gemm_tf32x3(Xh, Xl, Yh, Yl, d, ldp, ep, 0); cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -29,7 +31,8 @@ int main() {
     double ctas = h[2];
     printf("variant %d: ms %.3f ctas %.0f  per-CTA avg cycles: wait tmem_empty %.0f  wait full %.0f  mma loop %.0f\n",
            variant, ms, ctas, h[0] / ctas, h[1] / ctas, h[3] / ctas);
-    printf("  prologue %.0f  epilogue-final %.0f  start->drained %.0f  staged0 %.0f staged1 %.0f\n", h[4] / ctas, h[5] / ctas, h[6] / ctas, h[7] / ctas, h[8] / ctas);
+    unsigned long long h9; cudaMemcpy(&h9, dbg + 9, 8, cudaMemcpyDeviceToHost);
+    printf("  prologue %.0f  epilogue-final %.0f  start->drained %.0f  staged0 %.0f rowpass0-done %.0f staged1 %.0f\n", h[4] / ctas, h[5] / ctas, h[6] / ctas, h[7] / ctas, h9 / ctas, h[8] / ctas);
   }
   return 0;
 }
