@@ -37,8 +37,8 @@ namespace nseries {
 namespace {
 
 #ifndef NSERIES_TF32_BN
-#define NSERIES_TF32_BN 256
-#define NSERIES_TF32_BK 16
+#define NSERIES_TF32_BN 256   // (BN = 192 -- 4.76 waves instead of 3.46 at d = 4096 -- measured
+#define NSERIES_TF32_BK 16    //  11% slower: lower operand reuse per TMA byte)
 #define NSERIES_TF32_STAGES 4
 #endif
 #ifndef NSERIES_TF32_RU
@@ -62,7 +62,7 @@ constexpr int kFinalWarps = kThreads / 32;    // every warp runs the final epilo
 constexpr uint32_t kATileBytes = BM * BK * 4;   // 8 KB  (128 rows x 16 k)
 constexpr uint32_t kBTileBytes = BN * BK * 4;   // 8 KB (128 rows of Y^T x 16 k)
 constexpr uint32_t kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
-constexpr uint32_t kTmemCols = NBUF * BN;       // 512
+constexpr uint32_t kTmemCols = NBUF * BN <= 256 ? 256 : 512;   // allocation: power of two >= used
 constexpr uint32_t kSwizzleLayout = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / _64B
 constexpr uint32_t kAtomBytes = 8 * BK * 4;     // 8 rows x 64 B = 512 B (SBO)
 constexpr int kStageLd = EC + 1;                // epilogue staging row (floats)
@@ -497,8 +497,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       fence_after();
       const uint32_t t_acc = tmem + lane_off + b * BN + cb;
 #ifndef NSERIES_TF32_NO_DRAIN
+#if NSERIES_TF32_BN == 256
 #pragma unroll
-      for (int j = 0; j < EC / 32; j += 2) {
+      for (int j = 0; j < EC / 32; j += 2) {   // two 32-column loads in flight
         uint32_t v[32], w[32];
         tmem_ld32_async(t_acc + 32 * j, v);
         tmem_ld32_async(t_acc + 32 * (j + 1), w);
@@ -509,6 +510,20 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
           fadd2(acc[32 * (j + 1) + i], acc[32 * (j + 1) + i + 1], __uint_as_float(w[i]), __uint_as_float(w[i + 1]));
         }
       }
+#else
+#pragma unroll
+      for (int j = 0; j < EC / 32; ++j) {      // one 32-column group (two x16 loads) in flight
+        uint32_t v[16], w[16];
+        tmem_ld16_async(t_acc + 32 * j, v);
+        tmem_ld16_async(t_acc + 32 * j + 16, w);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          fadd2(acc[32 * j + i], acc[32 * j + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          fadd2(acc[32 * j + 16 + i], acc[32 * j + 16 + i + 1], __uint_as_float(w[i]), __uint_as_float(w[i + 1]));
+        }
+      }
+#endif
 #endif
       fence_before();
       if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
