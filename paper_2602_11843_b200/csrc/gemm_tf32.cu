@@ -41,10 +41,18 @@ namespace {
 #define NSERIES_TF32_BK 16    //  11% slower: lower operand reuse per TMA byte)
 #define NSERIES_TF32_STAGES 4
 #endif
+#ifndef NSERIES_TF32_CLUSTER
+#define NSERIES_TF32_CLUSTER 2   // CTA pairs along M share (TMA-multicast) the B operand tile
+#endif
 #ifndef NSERIES_TF32_RU
 #define NSERIES_TF32_RU 2   // rows per epilogue aux-load batch
 #endif
 constexpr int BM = 128, BN = NSERIES_TF32_BN, BK = NSERIES_TF32_BK, STAGES = NSERIES_TF32_STAGES;
+constexpr int CL = NSERIES_TF32_CLUSTER;     // 1 or 2 CTAs per cluster
+#ifndef NSERIES_TF32_PREFETCH
+#define NSERIES_TF32_PREFETCH 0   // (8 measured 19% slower at d = 4096: extra L2 traffic)
+#endif
+constexpr int kPrefetchKB = NSERIES_TF32_PREFETCH;   // L2 prefetch distance (k-blocks) of the producer
 // BK = 16 fp32 = 64-byte rows -> SWIZZLE_64B tiles (8-row atoms of 512 B).  Each 16-wide K
 // chunk is one accumulation unit; NBUF = 4 chunk accumulators keep 4 chunks (24 MMAs) queued
 // ahead of the drain round trip (commit -> epilogue tcgen05.ld -> arrive), which a 2-deep
@@ -129,6 +137,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// multicast variant: the box lands at the same shared offset in every CTA of ctaMask, and each
+// destination's mbarrier (same offset) receives the complete_tx
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(saddr(bar)), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -152,6 +184,12 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+// arrive on the mbarrier at the same offset in every CTA of ctaMask once the MMAs complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                   saddr(bar)), "h"(mask)
+               : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -358,7 +396,7 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(CL, 1, 1)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constant__ CUtensorMap mXl,
                    const __grid_constant__ CUtensorMap mYh, const __grid_constant__ CUtensorMap mYl,
                    int d, const __grid_constant__ EpiParamsF32 ep) {
@@ -366,7 +404,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = (d + BN - 1) / BN;
-  const int m0 = (blockIdx.x / ntn) * BM, n0 = (blockIdx.x % ntn) * BN;
+  // cluster of CL CTAs: same n0, consecutive row tiles; each CTA TMA-loads 1/CL of the B tile
+  // and multicasts it to the pair (a CTA whose rows fall past d still runs the protocol)
+  const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int pair = blockIdx.x / CL;
+  const int m0 = ((pair / ntn) * CL + rank) * BM, n0 = (pair % ntn) * BN;
   const int KB = (d + BK - 1) / BK;
   const int NC = KB * CPS;                   // accumulation chunks
 #ifdef NSERIES_TF32_DEBUG
@@ -375,7 +417,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CL); }
     for (int b = 0; b < NBUF; ++b) { mbar_init(&sm.tmem_full[b], 1); mbar_init(&sm.tmem_empty[b], kEpiWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -386,7 +428,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   fence_before();
-  __syncthreads();
+  if (CL > 1) cluster_sync_all();   // the peer's barriers are initialised before any multicast
+  else __syncthreads();
   fence_after();
   const uint32_t tmem = sm.tmem_base;
 
@@ -403,8 +446,21 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         const int k0 = kb * BK;
         tma_load_2d(sm.xh[s], &mXh, &sm.full[s], k0, m0);
         tma_load_2d(sm.xl[s], &mXl, &sm.full[s], k0, m0);
-        tma_load_2d(sm.yh[s], &mYh, &sm.full[s], k0, n0);   // Y^T rows n0..n0+BN-1
-        tma_load_2d(sm.yl[s], &mYl, &sm.full[s], k0, n0);
+        if (kPrefetchKB > 0 && kb + kPrefetchKB < KB) {   // pull a later k-block into L2 (DRAM latency)
+          const int kp = (kb + kPrefetchKB) * BK;
+          tma_prefetch_2d(&mXh, kp, m0);
+          tma_prefetch_2d(&mXl, kp, m0);
+          tma_prefetch_2d(&mYh, kp, n0 + rank * (BN / CL));
+          tma_prefetch_2d(&mYl, kp, n0 + rank * (BN / CL));
+        }
+        if (CL > 1) {   // this CTA's slice of Y^T rows n0 .. n0+BN-1, multicast to the pair
+          const int nb = rank * (BN / CL);
+          tma_load_2d_mc(sm.yh[s] + rank * (kBTileBytes / CL), &mYh, &sm.full[s], k0, n0 + nb, (1u << CL) - 1);
+          tma_load_2d_mc(sm.yl[s] + rank * (kBTileBytes / CL), &mYl, &sm.full[s], k0, n0 + nb, (1u << CL) - 1);
+        } else {
+          tma_load_2d(sm.yh[s], &mYh, &sm.full[s], k0, n0);   // Y^T rows n0..n0+BN-1
+          tma_load_2d(sm.yl[s], &mYl, &sm.full[s], k0, n0);
+        }
 #endif
       }
     }
@@ -460,7 +516,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
           }
           mma_commit(&sm.tmem_full[b]);        // chunk accumulator ready for the epilogue
         }
-        mma_commit(&sm.empty[s]);              // frees the smem stage once these MMAs finish
+        // frees the smem stage (in every CTA of the cluster: the pair multicasts into it) once
+        // these MMAs finish
+        if (CL > 1) mma_commit_mc(&sm.empty[s], (1u << CL) - 1);
+        else mma_commit(&sm.empty[s]);
       }
 #ifdef NSERIES_TF32_DEBUG
       if (g_dbg) {
@@ -564,7 +623,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   }
 #endif
   fence_before();
-  __syncthreads();
+  if (CL > 1) cluster_sync_all();   // no CTA leaves while its pair may still signal its barriers
+  else __syncthreads();
   if (warp == 2) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
@@ -644,7 +704,7 @@ int make_map(CUtensorMap* m, const float* base, int d, int ld, int role) {
   if (!enc) return (int)cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)d};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {(cuuint32_t)BK, role == 0 ? (cuuint32_t)BM : (cuuint32_t)BN};
+  cuuint32_t box[2] = {(cuuint32_t)BK, role == 0 ? (cuuint32_t)BM : (cuuint32_t)(BN / CL)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -688,8 +748,9 @@ int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const 
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
-  const int tiles = ((d + BM - 1) / BM) * ((d + BN - 1) / BN);
-  gemm_tf32x3_kernel<<<tiles, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(mxh, mxl, myh, myl, d, ep);
+  const int row_groups = ((d + BM - 1) / BM + CL - 1) / CL;   // clusters of CL row tiles
+  const int ctas = row_groups * ((d + BN - 1) / BN) * CL;
+  gemm_tf32x3_kernel<<<ctas, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(mxh, mxl, myh, myl, d, ep);
   return (int)cudaGetLastError();
 }
 
