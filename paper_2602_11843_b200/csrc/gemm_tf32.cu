@@ -471,55 +471,64 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       long long tstart = clock64();
       if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
 #endif
-      // The tensor pipe queues only a couple of MMAs, so any gap in issue longer than one MMA
-      // (64 cycles at N = 128) idles it.  Barrier state for the NEXT k-block / chunk is
-      // therefore probed with test_wait before this k-block's MMAs are issued and only
-      // waited on (rarely) afterwards; descriptors are built once per stage and advanced by
-      // adding the k-step offset to the start-address field.
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES, r = kb / STAGES;
+      // The tensor pipe queues only a couple of MMAs, so a blocking barrier wait between two
+      // chunks drains it (tools/tcgen05_rate.cu: 97 clk per N=128 MMA in a producer/consumer
+      // ring vs 64 back to back).  The barriers of the NEXT chunk (stage full, TMEM buffer
+      // empty) are therefore probed with a non-blocking test_wait right after this chunk's
+      // barriers are satisfied and BEFORE its MMAs are issued; the probe results are consumed
+      // one chunk later and a blocking wait happens only if a probe failed.
+      uint32_t full_ok = mbar_test(&sm.full[0], 0);
+      uint32_t tm_ok = 1;                        // chunk 0 uses a fresh buffer
+      for (int c = 0; c < NC; ++c) {
+        const int kb = c / CPS, h = c % CPS, s = kb % STAGES, r = kb / STAGES;
+        const int b = c % NBUF, u = c / NBUF;     // accumulator b, use count u
+        if (h == 0 && !full_ok) {
 #ifdef NSERIES_TF32_DEBUG
-        long long t1 = clock64();
+          long long t1 = clock64();
 #endif
-        mbar_wait(&sm.full[s], r & 1);
+          mbar_wait(&sm.full[s], r & 1);
 #ifdef NSERIES_TF32_DEBUG
-        if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
+          if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
 #endif
-        fence_after();
-        const uint64_t dxh = smem_desc(saddr(sm.xh[s]), 16, kAtomBytes), dxl = smem_desc(saddr(sm.xl[s]), 16, kAtomBytes);
-        const uint64_t dyh = smem_desc(saddr(sm.yh[s]), 16, kAtomBytes), dyl = smem_desc(saddr(sm.yl[s]), 16, kAtomBytes);
-#pragma unroll
-        for (int h = 0; h < CPS; ++h) {
-          const int c = kb * CPS + h;
-          const int b = c % NBUF, u = c / NBUF;   // accumulator b, use count u
+        }
+        if (u > 0 && !tm_ok) {
 #ifdef NSERIES_TF32_DEBUG
           long long t0 = clock64();
 #endif
-          if (u > 0) mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
+          mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
 #ifdef NSERIES_TF32_DEBUG
           if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
 #endif
-          fence_after();
-          const uint32_t t_acc = tmem + b * BN;
-          // small cross terms first (accumulator still small), hi*hi last; K-major swizzled
-          // tiles advance 32 B (8 tf32, +2 in the >>4 address field) per k-step
-#pragma unroll
-          for (int j = 0; j < KSC; ++j) {
-            const int ks = h * KSC + j;
-            mma_tf32(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
-            mma_tf32(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
-          }
-#pragma unroll
-          for (int j = 0; j < KSC; ++j) {
-            const int ks = h * KSC + j;
-            mma_tf32(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
-          }
-          mma_commit(&sm.tmem_full[b]);        // chunk accumulator ready for the epilogue
         }
-        // frees the smem stage (in every CTA of the cluster: the pair multicasts into it) once
-        // these MMAs finish
-        if (CL > 1) mma_commit_mc(&sm.empty[s], (1u << CL) - 1);
-        else mma_commit(&sm.empty[s]);
+        fence_after();
+        if (c + 1 < NC) {                         // probe the next chunk's barriers now
+          const int cn = c + 1, kbn = cn / CPS, bn = cn % NBUF, un = cn / NBUF;
+          full_ok = (cn % CPS) ? 1u : mbar_test(&sm.full[kbn % STAGES], (kbn / STAGES) & 1);
+          tm_ok = un == 0 ? 1u : mbar_test(&sm.tmem_empty[bn], (un - 1) & 1);
+        }
+        const uint64_t dxh = smem_desc(saddr(sm.xh[s]), 16, kAtomBytes), dxl = smem_desc(saddr(sm.xl[s]), 16, kAtomBytes);
+        const uint64_t dyh = smem_desc(saddr(sm.yh[s]), 16, kAtomBytes), dyl = smem_desc(saddr(sm.yl[s]), 16, kAtomBytes);
+        const uint32_t t_acc = tmem + b * BN;
+        // small cross terms first (accumulator still small), hi*hi last; K-major swizzled
+        // tiles advance 32 B (8 tf32, +2 in the >>4 address field) per k-step
+#pragma unroll
+        for (int j = 0; j < KSC; ++j) {
+          const int ks = h * KSC + j;
+          mma_tf32(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
+          mma_tf32(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
+        }
+#pragma unroll
+        for (int j = 0; j < KSC; ++j) {
+          const int ks = h * KSC + j;
+          mma_tf32(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
+        }
+        mma_commit(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
+        if (h == CPS - 1) {
+          // frees the smem stage (in every CTA of the cluster: the pair multicasts into it)
+          // once these MMAs finish
+          if (CL > 1) mma_commit_mc(&sm.empty[s], (1u << CL) - 1);
+          else mma_commit(&sm.empty[s]);
+        }
       }
 #ifdef NSERIES_TF32_DEBUG
       if (g_dbg) {

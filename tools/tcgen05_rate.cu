@@ -123,4 +123,9 @@ template <int STAGES> void run_ring(float* out) {
   printf("ring STAGES=%d: %.1f clk/instr  err=%s\n", STAGES, out[0], cudaGetErrorString(cudaGetLastError()));
 }
 int main() { float* out; cudaMallocManaged(&out, 64);
-  run_ring<2>(out); run_ring<4>(out); run_ring<6>(out); run_ring<12>(out); return 0; }
+  run<256, 64, 0>(out);   // back-to-back single MMAs
+  run<256, 64, 1>(out);   // 3-pass pattern, no commits
+  run<256, 64, 3>(out);   // 3-pass pattern, commit after every triple
+  run<128, 64, 1>(out);
+  run<128, 64, 3>(out);
+  run_ring<2>(out); run_ring<4>(out); return 0; }
