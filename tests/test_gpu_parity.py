@@ -247,8 +247,10 @@ def test_parity_f32_flags_and_R(h, steps, extra):
         assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-5
 
 
-@pytest.mark.parametrize("d", [5, 128, 300, 1024, 2048])
+@pytest.mark.parametrize("d", [5, 128, 300, 1024, 2048, 4100])
 def test_matmul_engine_f32(h, d):
+    # 4100: odd number of 128-row tiles (the second CTA of the last M-pair cluster lies past d)
+    # and a ragged last column tile
     # one 3xTF32 product vs the exact product of the fp32 inputs (<= 5e-7 budget)
     rng = np.random.default_rng(d + 7)
     X = rng.standard_normal((d, d)).astype(np.float32)
