@@ -242,14 +242,20 @@ def run_native(args):
         S32 = torch.empty_like(A32)
         for name, (stp, kk) in PLANS.items():
             fl = P.NSERIES_ALLOW_APPROX if 15 in stp else 0
-            n = max(2, args.steps // 2)
-            pms, pplan, _ = time_plan(P, h, A32, S32, stp, kk, n, 2, fl, stream, world)
+            n = max(4, args.steps)
+            with ClockSampler(local) as fclk:
+                pms, pplan, _ = time_plan(P, h, A32, S32, stp, kk, n, 2, fl, stream, world)
             pstep = pms / n
             alg = pplan.products * flop_per_product / (pstep * 1e-3) / 1e12
             per_plan[name + " fp32"] = {"k": kk, "products": pplan.products, "ms_per_eval": pstep,
                                         "evals_per_s": world * 1e3 / pstep, "tflops": alg,
                                         "tf32_tensor_tflops": 3 * alg,
-                                        "tf32_frac_of_peak": 3 * alg / TF32_PEAK_TFLOPS}
+                                        "tf32_frac_of_peak": 3 * alg / TF32_PEAK_TFLOPS,
+                                        "clocks": fclk.summary()}
+            c = per_plan[name + " fp32"]["clocks"]
+            if c.get("sm_mhz") and c.get("sm_max_mhz"):   # power-capped runs: peak at the clock held
+                per_plan[name + " fp32"]["tf32_frac_of_peak_at_held_clock"] = (
+                    3 * alg / (TF32_PEAK_TFLOPS * c["sm_mhz"] / c["sm_max_mhz"]))
         del A32, S32
 
     configs = None
