@@ -232,6 +232,16 @@ def run_native(args):
             per_plan[name] = {"k": kk, "products": pplan.products, "ms_per_eval": pstep,
                               "evals_per_s": world * 1e3 / pstep,
                               "tflops": pplan.products * flop_per_product / (pstep * 1e-3) / 1e12}
+        # NSERIES_SYMMETRIC (config 3's A is symmetric): same products, upper-triangle tiles only
+        for name, (stp, kk) in PLANS.items():
+            fl = (P.NSERIES_ALLOW_APPROX if 15 in stp else 0) | P.NSERIES_SYMMETRIC
+            n = max(2, args.steps // 2)
+            pms, pplan, _ = time_plan(P, h, A, S, stp, kk, n, 2, fl, stream, world)
+            pstep = pms / n
+            per_plan[name + " fp64 symmetric"] = {
+                "k": kk, "products": pplan.products, "ms_per_eval": pstep, "evals_per_s": world * 1e3 / pstep,
+                "tflops_dense_equivalent": pplan.products * flop_per_product / (pstep * 1e-3) / 1e12,
+                "tflops_executed": pplan.products * flop_per_product * _sym_fraction(D) / (pstep * 1e-3) / 1e12}
         b = per_plan["x2^12"]
         for name in ("x15^3", "x9^4"):
             p = per_plan[name]
@@ -312,6 +322,12 @@ def run_native(args):
         print(json.dumps(line), flush=True)
     R.teardown(world)
     return 0
+
+
+def _sym_fraction(d, bm=128):
+    """Fraction of the dense tile work the symmetric mode executes (tiles on/above the diagonal)."""
+    nt = -(-d // bm)
+    return (nt * (nt + 1) / 2) / (nt * nt)
 
 
 def _time_evals(fn, n, n_warm, stream):

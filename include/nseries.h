@@ -84,6 +84,11 @@ typedef enum {
                                          of the paper's R' = I - M Y' (PAPER.md:557 vs 573)   */
 #define NSERIES_NO_GRAPH         0x8u /* do not capture/replay the op list as a CUDA graph     */
 #define NSERIES_SYNC_STATS       0x10u/* record per-op CUDA events for nseries_last_stats      */
+#define NSERIES_SYMMETRIC        0x20u/* caller asserts A = A^T (fp64, d > 64): every value of
+                                         the plan is a polynomial in A, hence symmetric, so each
+                                         product computes only the tiles on/above the diagonal and
+                                         mirrors them (same products, ~half the tile work).  The
+                                         result is unspecified if A is not symmetric.           */
 
 #define NSERIES_MAX_STEPS 128
 

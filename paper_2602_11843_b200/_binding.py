@@ -22,6 +22,7 @@ NSERIES_ALLOW_APPROX = 0x2
 NSERIES_RFORM_TELESCOPE = 0x4
 NSERIES_NO_GRAPH = 0x8
 NSERIES_SYNC_STATS = 0x10
+NSERIES_SYMMETRIC = 0x20
 NSERIES_MAX_STEPS = 128
 
 # every symbol include/nseries.h declares (tests check the .so exports exactly these)

@@ -218,7 +218,8 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
 // fused sum-of-squares reduction of output sumsq_out of op sumsq_op.
 nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
                                  int d, cudaStream_t s, int i0, int i1, int* launches,
-                                 int sumsq_op = -1, int sumsq_out = -1, double* sumsq_ptr = nullptr) {
+                                 int sumsq_op = -1, int sumsq_out = -1, double* sumsq_ptr = nullptr,
+                                 bool sym = false) {
   const size_t slot = (size_t)d * d * sizeof(double);
   auto ptr = [&](int v) -> void* {
     switch (P.val_kind[v]) {
@@ -246,6 +247,7 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
       ep.sumsq = sumsq_ptr;
       ep.sumsq_out = sumsq_out;
     }
+    ep.sym = sym ? 1 : 0;
     const int rc = op.gemm ? launch_gemm_f64(static_cast<const double*>(ptr(op.X)),
                                              static_cast<const double*>(ptr(op.Y)), d, ep, s)
                            : launch_axpby_f64(d, ep, s);
@@ -259,7 +261,7 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
 // Execute a compiled program on the stream.  fp64 with d <= 64: the whole op list runs in one
 // single-CTA launch (plan_small.cu); otherwise one tiled GEMM launch per op.
 nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
-                           int d, nseries_dtype dt, cudaStream_t s, int* launches) {
+                           int d, nseries_dtype dt, cudaStream_t s, int* launches, bool sym = false) {
   if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
   if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode == 0) {
     // 4-CTA cluster, each CTA a 16-row block of every value (DSMEM for the operand rows)
@@ -321,7 +323,7 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
     *launches = 1;
     return NSERIES_OK;
   }
-  return run_program_range(h, P, A, S, R, d, s, 0, (int)P.ops.size(), launches);
+  return run_program_range(h, P, A, S, R, d, s, 0, (int)P.ops.size(), launches, -1, -1, nullptr, sym);
 }
 
 }  // namespace
@@ -448,7 +450,7 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   int launches = 0;
   auto run = [&](cudaStream_t st_) {
     return dt == NSERIES_F64
-               ? run_program(h, P, A, S, R_out, d, dt, st_, &launches)
+               ? run_program(h, P, A, S, R_out, d, dt, st_, &launches, (flags & NSERIES_SYMMETRIC) != 0)
                : run_program_f32(h, P, static_cast<const float*>(A), static_cast<float*>(S),
                                  static_cast<float*>(R_out), d, st_, &launches);
   };
@@ -456,8 +458,9 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   if (!(flags & NSERIES_NO_GRAPH)) {
     // The op list is replayed as one CUDA graph: the pointers are baked in, so the key holds
     // them; capture runs on a private stream (the caller's may be the legacy NULL stream).
-    char ptrs[96];
-    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p", d, (int)dt, A, S, R_out, h->ws, h->ident);
+    char ptrs[192];
+    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
+                  (flags & NSERIES_SYMMETRIC) ? 1 : 0);
     const std::string gkey = key + ptrs;
     auto git = h->graphs.find(gkey);
     if (git == h->graphs.end()) {

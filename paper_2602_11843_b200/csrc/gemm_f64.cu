@@ -63,7 +63,7 @@ struct Cfg {
   static constexpr size_t kSmem = (size_t)STAGES * (kStageA + kStageB) * sizeof(double);
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2, bool SYM>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::kThreads, 1)
 gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, EpiParams ep) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
@@ -75,12 +75,26 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
   constexpr int GROUP = 8;
   const int ntm = (d + BM - 1) / BM, ntn = (d + BN - 1) / BN;
   const int pid = blockIdx.x;
-  const int band = GROUP * ntn;
-  const int first_tm = (pid / band) * GROUP;
-  const int gsz = min(ntm - first_tm, GROUP);
-  const int tm = first_tm + (pid % band) % gsz;
-  const int tn = (pid % band) / gsz;
+  int tm, tn;
+  if constexpr (SYM) {
+    // symmetric mode (BM == BN): the upper triangle tm <= tn, row after row
+    int rem = pid, r = 0;
+    while (rem >= ntn - r) { rem -= ntn - r; ++r; }
+    tm = r;
+    tn = r + rem;
+  } else {
+    const int band = GROUP * ntn;
+    const int first_tm = (pid / band) * GROUP;
+    const int gsz = min(ntm - first_tm, GROUP);
+    tm = first_tm + (pid % band) % gsz;
+    tn = (pid % band) / gsz;
+  }
   const int m0 = tm * BM, n0 = tn * BN;
+  // symmetric mode: an off-diagonal tile is also stored transposed; inside a diagonal tile the
+  // strictly upper elements are stored at both positions and the strictly lower ones are not
+  // stored at all, so every output is exactly symmetric
+  const bool mirror = SYM && tm != tn;
+  const bool diag_tile = SYM && tm == tn;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / C::kWarpsN) * WM, wn0 = (warp % C::kWarpsN) * WN;
@@ -210,8 +224,26 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
             if (x < n_aux) { v0 += ep.beta[o][x] * av[x].x; v1 += ep.beta[o][x] * av[x].y; }
           if (row == col) v0 += ep.gamma[o];
           if (row == col + 1) v1 += ep.gamma[o];
-          if (o == ep.sumsq_out) ssq += v0 * v0 + v1 * v1;
-          *reinterpret_cast<double2*>(static_cast<double*>(ep.out[o]) + off) = make_double2(v0, v1);
+          double* const od = static_cast<double*>(ep.out[o]);
+          if (!diag_tile) {
+            if (o == ep.sumsq_out) ssq += (mirror ? 2.0 : 1.0) * (v0 * v0 + v1 * v1);
+            *reinterpret_cast<double2*>(od + off) = make_double2(v0, v1);
+            if (mirror) {
+              od[(size_t)col * d + row] = v0;
+              od[(size_t)(col + 1) * d + row] = v1;
+            }
+          } else {
+            if (row <= col) {
+              od[off] = v0;
+              od[(size_t)col * d + row] = v0;
+              if (o == ep.sumsq_out) ssq += (row == col ? 1.0 : 2.0) * v0 * v0;
+            }
+            if (row <= col + 1) {
+              od[off + 1] = v1;
+              od[(size_t)(col + 1) * d + row] = v1;
+              if (o == ep.sumsq_out) ssq += (row == col + 1 ? 1.0 : 2.0) * v1 * v1;
+            }
+          }
         }
       } else {
 #pragma unroll
@@ -229,8 +261,11 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
             for (int x = 0; x < kMaxAux; ++x)
               if (x < n_aux) v += ep.beta[o][x] * av[x];
             if (row == col + e) v += ep.gamma[o];
-            if (o == ep.sumsq_out) ssq += v * v;
+            if (diag_tile && row > col + e) continue;   // written by its mirror element
+            const bool twice = mirror || (diag_tile && row < col + e);
+            if (o == ep.sumsq_out) ssq += (twice ? 2.0 : 1.0) * v * v;
             static_cast<double*>(ep.out[o])[off + e] = v;
+            if (twice) static_cast<double*>(ep.out[o])[(size_t)(col + e) * d + row] = v;
           }
         }
       }
@@ -266,10 +301,10 @@ __global__ void identity_f64_kernel(double* I, int d) {
     I[idx] = (idx / d == idx % d) ? 1.0 : 0.0;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2>
-int launch_cfg(const double* X, const double* Y, int d, const EpiParams& ep, cudaStream_t s) {
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2, bool SYM>
+int launch_cfg_t(const double* X, const double* Y, int d, const EpiParams& ep, cudaStream_t s) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
-  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2>;
+  auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2, SYM>;
   static bool attr_set = false;   // per template instance
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -277,9 +312,18 @@ int launch_cfg(const double* X, const double* Y, int d, const EpiParams& ep, cud
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  const int tiles = ((d + BM - 1) / BM) * ((d + BN - 1) / BN);
+  const int nt = (d + BM - 1) / BM;
+  static_assert(BM == BN, "symmetric mode assumes square tiles");
+  const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ((d + BN - 1) / BN);
   kern<<<tiles, C::kThreads, C::kSmem, s>>>(X, Y, d, ep);
   return (int)cudaGetLastError();
+}
+
+// the symmetric variant is a separate instantiation: the general kernel is unchanged by it
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2>
+int launch_cfg(const double* X, const double* Y, int d, const EpiParams& ep, cudaStream_t s) {
+  return ep.sym ? launch_cfg_t<BM, BN, BK, WM, WN, STAGES, V2, true>(X, Y, d, ep, s)
+                : launch_cfg_t<BM, BN, BK, WM, WN, STAGES, V2, false>(X, Y, d, ep, s);
 }
 
 }  // namespace
@@ -291,7 +335,8 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   for (int i = 0; i < ep.n_out; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.out[i]) % 16 == 0;
   // Tile choice by wave efficiency: 128x128 (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs,
   // weighted by each config's measured per-SM efficiency (0.93 vs 0.82 of DMMA peak).
-  const double tb = std::ceil(d / 128.0) * std::ceil(d / 128.0), ts = std::ceil(d / 64.0) * std::ceil(d / 64.0);
+  const double nb = std::ceil(d / 128.0), ns = std::ceil(d / 64.0);
+  const double tb = ep.sym ? nb * (nb + 1) / 2 : nb * nb, ts = ep.sym ? ns * (ns + 1) / 2 : ns * ns;
   const double eb = 0.93 * tb / (std::ceil(tb / 148.0) * 148.0);
   const double es = 0.82 * ts / (std::ceil(ts / 296.0) * 296.0);
   if (eb >= es) {

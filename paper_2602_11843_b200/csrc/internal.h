@@ -82,6 +82,9 @@ struct EpiParams {
   double gamma[kMaxOut];
   double* sumsq = nullptr;       // optional: atomically accumulate sum of squares of out[sumsq_out]
   int sumsq_out = -1;
+  int sym = 0;                   // symmetric mode: X, Y, aux and outputs are symmetric (polynomials
+                                 // of a symmetric A); only tiles on/above the diagonal are computed
+                                 // and each off-diagonal output tile is also stored transposed
 };
 
 // Batched small-matrix path: the compiled op list with values mapped to shared-memory slots.

@@ -189,12 +189,15 @@ def test_config2_probes(h, steps):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("sym", [0, 1])
 @pytest.mark.parametrize("steps", [[15, 15, 15], [9, 9, 9, 9], [2] * 12])
-def test_config3_probes(h, steps):
+def test_config3_probes(h, steps, sym):
+    # config 3's A is symmetric by construction: also through NSERIES_SYMMETRIC
     A_dev, _, _ = inputs.cfg3(device="cuda")
     A = A_dev.cpu().numpy()
+    assert np.array_equal(A, A.T)
     V, _ = inputs.probe_block(A.shape[0], 2, n_unit=1, n_gauss=1)
-    S, R, _ = _run(h, A, steps, want_R=True)
+    S, R, _ = _run(h, A, steps, flags=P.NSERIES_SYMMETRIC if sym else 0, want_R=True)
     assert _probe_parity(S, A, steps, V, 15 in steps) <= TOL64
     # property at full size: (I - A) S = I - R  (Lemma 5 / telescoping), checked on probes
     lhs = O.matvec(S, V) - O.matvec(A, np.asarray(O.matvec(S, V), dtype=np.float64))
@@ -311,3 +314,25 @@ def test_small_kernels_flags_and_R(h_small_modes, d, steps, extra, which):
     assert O.rel_fro(S, Sref) <= TOL64, (d, steps, flags, which)
     scale = float(np.sqrt(np.sum(np.asarray(Sref, dtype=LD) ** 2)))
     assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-13
+
+
+
+@pytest.mark.parametrize("d", [65, 130, 300, 513, 1024])
+@pytest.mark.parametrize("steps,extra", [([9, 9], 0), ([15, 15], 0), ([15, 1, 5], 2), ([2] * 5, 1),
+                                         ([5, 5], 0), ([3, 1, 9], 0)])
+def test_symmetric_mode(h, d, steps, extra):
+    # NSERIES_SYMMETRIC: upper-triangle tiles + mirrored stores (fp64 tiled engine, d > 64);
+    # odd d exercises the scalar-store path; R_out and the residual form included
+    flags = [0, P.NSERIES_ELIDE_TRIVIAL, P.NSERIES_RFORM_TELESCOPE][extra] | P.NSERIES_SYMMETRIC
+    G = inputs.random_matrix(d, 500 + d, 0.7)
+    A = 0.5 * (G + G.T)
+    S, R, st = _run(h, A, steps, flags=flags, want_R=True)
+    assert np.array_equal(S, S.T) and np.array_equal(R, R.T)        # mirrored, bit for bit
+    Sref, Rref = _oracle_full(A, steps, want_R=True)
+    assert O.rel_fro(S, Sref) <= TOL64, (d, steps, flags)
+    scale = float(np.sqrt(np.sum(np.asarray(Sref, dtype=LD) ** 2)))
+    assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-13
+    # same products as the general path
+    S2, _, st2 = _run(h, A, steps, flags=flags & ~P.NSERIES_SYMMETRIC, want_R=True)
+    assert st["products"] == st2["products"]
+    assert O.rel_fro(S, S2) <= 1e-13
