@@ -262,6 +262,13 @@ def run_native(args):
                                         "tf32_tensor_tflops": 3 * alg,
                                         "tf32_frac_of_peak": 3 * alg / TF32_PEAK_TFLOPS,
                                         "clocks": fclk.summary()}
+            with ClockSampler(local) as sclk:
+                sms, _, _ = time_plan(P, h, A32, S32, stp, kk, n, 2, fl | P.NSERIES_SYMMETRIC, stream, world)
+            sstep = sms / n
+            per_plan[name + " fp32 symmetric"] = {
+                "k": kk, "products": pplan.products, "ms_per_eval": sstep, "evals_per_s": world * 1e3 / sstep,
+                "tflops_dense_equivalent": pplan.products * flop_per_product / (sstep * 1e-3) / 1e12,
+                "clocks": sclk.summary()}
             c = per_plan[name + " fp32"]["clocks"]
             if c.get("sm_mhz") and c.get("sm_max_mhz"):   # power-capped runs: peak at the clock held
                 per_plan[name + " fp32"]["tf32_frac_of_peak_at_held_clock"] = (

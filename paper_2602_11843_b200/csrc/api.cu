@@ -120,7 +120,7 @@ size_t f32_ws_bytes(const Program& P, int d) {
 }
 
 nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A, float* S, float* R,
-                               int d, cudaStream_t s, int* launches) {
+                               int d, cudaStream_t s, int* launches, bool sym = false) {
   const int ldp = padded_ld(d);
   const size_t plane = (size_t)d * ldp;
   float* ws = static_cast<float*>(h->ws);
@@ -137,7 +137,7 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
     int l = op.X, r = op.Y;
     if (cost(op.Y, op.X) < cost(op.X, op.Y)) std::swap(l, r);
     role[l] |= 1;
-    role[r] |= 2;
+    role[r] |= sym ? 1 : 2;   // symmetric values: the right factor reads the row-major planes
     lr[i] = {l, r};
   }
   auto slot_of = [&](int v) -> int {
@@ -163,8 +163,8 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
   float* id_lo = id_hi + plane;
   auto hi = [&](int v) { return P.val_kind[v] == V_IDENT ? id_hi : planes(v) + plane; };
   auto lo = [&](int v) { return P.val_kind[v] == V_IDENT ? id_lo : planes(v) + 2 * plane; };
-  auto hiT = [&](int v) { return P.val_kind[v] == V_IDENT ? id_hi : planes(v) + 3 * plane; };
-  auto loT = [&](int v) { return P.val_kind[v] == V_IDENT ? id_lo : planes(v) + 4 * plane; };
+  auto hiT = [&](int v) { return P.val_kind[v] == V_IDENT ? id_hi : planes(v) + (sym ? 1 : 3) * plane; };
+  auto loT = [&](int v) { return P.val_kind[v] == V_IDENT ? id_lo : planes(v) + (sym ? 2 : 4) * plane; };
   int nl = 0;
   const int vA = 0;
   if (role[vA]) {   // one-off split of the user's A into the engine's operand planes
@@ -185,6 +185,7 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
     ep.n_aux = op.n_aux;
     ep.n_out = op.n_out;
     ep.ldp = ldp;
+    ep.sym = (sym && op.gemm) ? 1 : 0;
     for (int a = 0; a < op.n_aux; ++a) ep.aux[a] = xplane(op.aux[a], &ep.aux_ld[a]);
     for (int j = 0; j < op.n_out; ++j) {
       const int v = op.out[j];
@@ -452,7 +453,8 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     return dt == NSERIES_F64
                ? run_program(h, P, A, S, R_out, d, dt, st_, &launches, (flags & NSERIES_SYMMETRIC) != 0)
                : run_program_f32(h, P, static_cast<const float*>(A), static_cast<float*>(S),
-                                 static_cast<float*>(R_out), d, st_, &launches);
+                                 static_cast<float*>(R_out), d, st_, &launches,
+                                 (flags & NSERIES_SYMMETRIC) != 0);
   };
   bool replayed = false;
   if (!(flags & NSERIES_NO_GRAPH)) {

@@ -272,7 +272,7 @@ __device__ float* g_dbg = nullptr;
 template <int NO>   // number of outputs (compile-time: the per-element loops fully unroll)
 __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const int m0, const int n0, const int d,
                                            const int ew, const int lane, const EpiParamsF32& ep,
-                                           const int warp, const long long t_drained) {
+                                           const int warp, const long long t_drained, const bool diag_pair) {
   // re-derive the staging pointer from the dynamic shared array so that accesses compile to
   // LDS / STS (a generic pointer passed in would not)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -303,7 +303,7 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
     for (int pass = 0, tnext = 0; pass < 1 + kMaxOut; ++pass) {
       int tout = -1;                         // output staged for the column pass in this pass
       for (int o = tnext; o < n_out; ++o)
-        if (ep.out_hiT[o]) { tout = o; break; }
+        if (ep.sym || ep.out_hiT[o]) { tout = o; break; }
       if (pass > 0 && tout < 0) break;
       tnext = tout + 1;
       float al[kMaxOut], ga[kMaxOut], be[kMaxOut][kMaxAux];
@@ -357,11 +357,13 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
 #pragma unroll
               for (int x = 0; x < kMaxAux; ++x) t = fmaf(be[o][x], av[u][cc][x], t);   // be = 0 beyond n_aux
               if (cl == dcol) t += ga[o];
-              if (ox[o]) ox[o][(size_t)r * old_[o] + hn0 + cl] = t;
-              if (oh[o]) {
-                const float hi = rna_tf32_fast(t);
-                oh[o][(size_t)r * ldp + hn0 + cl] = hi;
-                ol[o][(size_t)r * ldp + hn0 + cl] = rna_tf32_fast(t - hi);
+              if (!diag_pair || cl >= dcol) {   // symmetric diagonal tiles: upper part only
+                if (ox[o]) ox[o][(size_t)r * old_[o] + hn0 + cl] = t;
+                if (oh[o]) {
+                  const float hi = rna_tf32_fast(t);
+                  oh[o][(size_t)r * ldp + hn0 + cl] = hi;
+                  ol[o][(size_t)r * ldp + hn0 + cl] = rna_tf32_fast(t - hi);
+                }
               }
               if (o == tout) vt[rr * kStageLd + cl] = t;
             }
@@ -372,7 +374,31 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
       if (warp == 4 && lane == 0 && g_dbg && hh == 0 && pass == 0)
         atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 9, (unsigned long long)(clock64() - t_drained));
 #endif
-      if (tout >= 0) {
+      if (tout >= 0 && ep.sym) {
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
+        // symmetric mode: the mirror image (c, r) of every element (r, c) (strictly upper part
+        // in diagonal tiles) into the output's own x / hi / lo planes; lanes along rows
+        float* const mx = ep.out_x[tout];
+        float* const mh = ep.out_hi[tout];
+        float* const ml = ep.out_lo[tout];
+        const int mld = ep.out_ld[tout];
+        for (int cl = ew; cl < ncol; cl += kFinalWarps) {
+          const int c = hn0 + cl;
+#pragma unroll
+          for (int rc = 0; rc < BM / 32; ++rc) {
+            const int rr = rc * 32 + lane, r = m0 + rr;
+            if (rr >= nrow) break;
+            if (diag_pair && r >= c) continue;
+            const float v = vt[rr * kStageLd + cl];
+            if (mx) mx[(size_t)c * mld + r] = v;
+            if (mh) {
+              const float hi = rna_tf32_fast(v);
+              mh[(size_t)c * ldp + r] = hi;
+              ml[(size_t)c * ldp + r] = rna_tf32_fast(v - hi);
+            }
+          }
+        }
+      } else if (tout >= 0) {
         asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
         // column pass: transposed operand planes, lanes along rows of the tile
         float* const ohT = ep.out_hiT[tout];
@@ -408,7 +434,21 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   // and multicasts it to the pair (a CTA whose rows fall past d still runs the protocol)
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
   const int pair = blockIdx.x / CL;
-  const int m0 = ((pair / ntn) * CL + rank) * BM, n0 = (pair % ntn) * BN;
+  int m0, n0;
+  bool diag_pair = false;
+  if (ep.sym) {
+    // symmetric mode (CL * BM == BN): square CL*BM x BN pair tiles on/above the diagonal,
+    // enumerated row after row
+    int rem = pair, pr = 0;
+    while (rem >= ntn - pr) { rem -= ntn - pr; ++pr; }
+    const int tn = pr + rem;
+    m0 = (pr * CL + rank) * BM;
+    n0 = tn * BN;
+    diag_pair = tn == pr;
+  } else {
+    m0 = ((pair / ntn) * CL + rank) * BM;
+    n0 = (pair % ntn) * BN;
+  }
   const int KB = (d + BK - 1) / BK;
   const int NC = KB * CPS;                   // accumulation chunks
 #ifdef NSERIES_TF32_DEBUG
@@ -621,9 +661,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
     const uint32_t tiles_off = (uint32_t)(reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw);
     const int ew = warp >= 4 ? warp - 4 : warp + kEpiWarps;   // 0..11
-    if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
-    else if (ep.n_out == 2) tile_epilogue<2>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
-    else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td);
+    if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
+    else if (ep.n_out == 2) tile_epilogue<2>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
+    else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
   }
 #ifdef NSERIES_TF32_DEBUG
   if (warp == 4 && lane == 0 && g_dbg) {
@@ -758,7 +798,9 @@ int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const 
     attr = true;
   }
   const int row_groups = ((d + BM - 1) / BM + CL - 1) / CL;   // clusters of CL row tiles
-  const int ctas = row_groups * ((d + BN - 1) / BN) * CL;
+  const int ntn = (d + BN - 1) / BN;
+  if (ep.sym && CL * BM != BN) return (int)cudaErrorInvalidValue;   // square pair tiles needed
+  const int ctas = ep.sym ? ntn * (ntn + 1) / 2 * CL : row_groups * ntn * CL;
   gemm_tf32x3_kernel<<<ctas, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(mxh, mxl, myh, myl, d, ep);
   return (int)cudaGetLastError();
 }

@@ -148,6 +148,9 @@ struct EpiParamsF32 {
   float* out_loT[kMaxOut];
   int out_ld[kMaxOut];          // leading dimension of out_x (operand planes use ldp)
   int ldp;
+  int sym;                      // symmetric mode: upper-triangle 256x256 pair tiles only; every
+                                // output's x / hi / lo planes are also stored mirrored (no
+                                // transposed operand planes: Y^T = Y for symmetric values)
   double alpha[kMaxOut];          // binary64: the epilogue combines in double, rounds once
   double beta[kMaxOut][kMaxAux];
   double gamma[kMaxOut];

@@ -189,8 +189,7 @@ def test_config2_probes(h, steps):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("sym", [0, 1])
-@pytest.mark.parametrize("steps", [[15, 15, 15], [9, 9, 9, 9], [2] * 12])
+@pytest.mark.parametrize("steps,sym", [([15, 15, 15], 0), ([9, 9, 9, 9], 0), ([2] * 12, 0), ([15, 15, 15], 1)])
 def test_config3_probes(h, steps, sym):
     # config 3's A is symmetric by construction: also through NSERIES_SYMMETRIC
     A_dev, _, _ = inputs.cfg3(device="cuda")
@@ -268,13 +267,13 @@ def test_matmul_engine_f32(h, d):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("steps", [[15, 15, 15], [9, 9, 9, 9], [2] * 12])
-def test_config3_probes_f32(h, steps):
+@pytest.mark.parametrize("steps,sym", [([15, 15, 15], 0), ([9, 9, 9, 9], 0), ([2] * 12, 0), ([15, 15, 15], 1)])
+def test_config3_probes_f32(h, steps, sym):
     A_dev, _, _ = inputs.cfg3(device="cuda")
     A32 = A_dev.float()
     A = A32.double().cpu().numpy()                     # fl32(A), exactly what the GPU sees
     V, _ = inputs.probe_block(A.shape[0], 2, n_unit=1, n_gauss=1)
-    S, _, _ = _run(h, A, steps, dtype=torch.float32)
+    S, _, _ = _run(h, A, steps, flags=P.NSERIES_SYMMETRIC if sym else 0, dtype=torch.float32)
     # at the fp32 tolerance the S_k oracle also bounds the radix-15 deviation (1.7e-8)
     assert _probe_parity(S.astype(np.float64), A, steps, V, 15 in steps) <= TOL32
 
@@ -336,3 +335,20 @@ def test_symmetric_mode(h, d, steps, extra):
     S2, _, st2 = _run(h, A, steps, flags=flags & ~P.NSERIES_SYMMETRIC, want_R=True)
     assert st["products"] == st2["products"]
     assert O.rel_fro(S, S2) <= 1e-13
+
+
+@pytest.mark.parametrize("d", [100, 300, 512, 1000])
+@pytest.mark.parametrize("steps,extra", [([9, 9], 0), ([15, 15], 0), ([15, 1, 5], 1), ([2] * 5, 0),
+                                         ([5, 5], 1), ([3, 1, 9], 0)])
+def test_symmetric_mode_f32(h, d, steps, extra):
+    # fp32 engine with NSERIES_SYMMETRIC: upper-triangle 256x256 pair tiles, mirrored x/hi/lo
+    # planes (no transposed operand planes); tolerance 2e-5 against the oracle on fl32(A)
+    flags = [0, P.NSERIES_ELIDE_TRIVIAL][extra] | P.NSERIES_SYMMETRIC
+    G = inputs.random_matrix(d, 700 + d, 0.7)
+    A = (0.5 * (G + G.T)).astype(np.float32).astype(np.float64)
+    S, R, _ = _run(h, A, steps, flags=flags, want_R=True, dtype=torch.float32)
+    assert np.array_equal(S, S.T) and np.array_equal(R, R.T)
+    Sref = _oracle_full(A, steps)
+    assert O.rel_fro(S.astype(np.float64), Sref) <= 2e-5, (d, steps, flags)
+    S2, _, _ = _run(h, A, steps, flags=flags & ~P.NSERIES_SYMMETRIC, dtype=torch.float32)
+    assert O.rel_fro(S.astype(np.float64), S2.astype(np.float64)) <= 2e-5
