@@ -125,7 +125,7 @@ __device__ __forceinline__ uint32_t mbar_test(uint64_t* b, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   // bounded spin: a protocol bug traps instead of hanging the device
   for (uint32_t i = 0; !mbar_try_wait(b, parity); ++i)
-    if (i > (1u << 30)) __trap();
+    if (i > (1u << 26)) __trap();
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
