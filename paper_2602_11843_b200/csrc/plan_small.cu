@@ -265,7 +265,7 @@ int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double
 namespace nseries {
 namespace {
 
-constexpr int kClusterCtas = 4, kRowsPerCta = 64 / kClusterCtas;     // 16
+constexpr int kClusterCtas = 8, kRowsPerCta = 64 / kClusterCtas;     // default cluster: 8 x 8 rows (25 us vs 29 at 4, 36 at 2)
 #ifdef NSERIES_SMALL_PROFILE
 __device__ long long g_small_prof[256];
 #endif
@@ -279,20 +279,22 @@ struct __align__(16) ClusterOp {
   int aux[kMaxAux], out[kMaxOut];                      // offsets (doubles); out < 0: not kept
 };
 
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(256, 1)
+template <int NC>   // CTAs per cluster; each owns RPC = 64 / NC rows of every value
+__global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(256, 1)
 plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S, double* __restrict__ R,
                         const __grid_constant__ WarpProgram prog) {
+  constexpr int RPC = 64 / NC, MB = RPC / 8, kCSlotD = RPC * 64;
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double smc[];
   const int rank = (int)cluster.block_rank();
-  const int r0 = rank * kRowsPerCta;
+  const int r0 = rank * RPC;
   const int n_ops = prog.n_ops;
   double* const sA = smc + prog.n_slots * kCSlotD;
   ClusterOp* const sops = reinterpret_cast<ClusterOp*>(smc + (prog.n_slots + 1) * kCSlotD);
-  const double* peer[kClusterCtas];
+  const double* peer[NC];
 #pragma unroll
-  for (int c = 0; c < kClusterCtas; ++c) peer[c] = cluster.map_shared_rank(smc, c);
+  for (int c = 0; c < NC; ++c) peer[c] = cluster.map_shared_rank(smc, c);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wn0 = warp * 8;            // 8 warps x 8 output columns; each warp all 16 local rows
@@ -334,38 +336,38 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     // KS independent partial accumulators per row block (k-steps s with s % KS == p) keep KS
     // DMMA chains in flight per row block instead of one 16-long dependent chain
     constexpr int KS = 4;
-    double part[2][KS][2];
+    double part[MB][KS][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < MB; ++i)
 #pragma unroll
       for (int p = 0; p < KS; ++p) part[i][p][0] = part[i][p][1] = 0.0;
     const int kind = op.kind;
     if (kind != 0) {
       const bool xi = kind == 2, yi = kind == 3;
       const int xo = op.x, yo = op.y;
-      // B fragments: Y[k + t][wn0 + g] for the 16 k-steps, rows owned by CTA (k + t) / 16;
+      // B fragments: Y[k + t][wn0 + g] for the 16 k-steps, rows owned by CTA (k + t) / RPC;
       // all issued before the first MMA (remote latency)
       double bf[16];
       const int col = wn0 + g;
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const int k = 4 * s + t;
-        bf[s] = yi ? ((k == col && col < d) ? 1.0 : 0.0) : peer[k >> 4][yo + swz64(k & 15, col)];
+        bf[s] = yi ? ((k == col && col < d) ? 1.0 : 0.0) : peer[k / RPC][yo + swz64(k % RPC, col)];
       }
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const int k = 4 * s + t;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < MB; ++i) {
           const int rl = i * 8 + g;
           const double a = xi ? ((r0 + rl == k && r0 + rl < d) ? 1.0 : 0.0) : smc[xo + swz64(rl, k)];
           dmma884(part[i][s % KS], a, bf[s]);
         }
       }
     }
-    double acc[2][2];
+    double acc[MB][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < MB; ++i)
 #pragma unroll
       for (int e = 0; e < 2; ++e) acc[i][e] = (part[i][0][e] + part[i][1][e]) + (part[i][2][e] + part[i][3][e]);
 #ifdef NSERIES_SMALL_PROFILE
@@ -374,7 +376,7 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     // epilogue on local rows (no barrier needed before it: outputs never alias this op's operands)
     const int n_aux = op.n_aux, n_out = op.n_out;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < MB; ++i) {
       const int rl = i * 8 + g, row = r0 + rl;
       const int colp = wn0 + 2 * t;
       const int off = swz64(rl, colp);
@@ -411,16 +413,26 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
   }
 }
 
+template <int NC>
+int launch_cluster_nc(int d, const WarpProgram& prog, const double* A, double* S, double* R, cudaStream_t stream) {
+  constexpr int kCSlotD = (64 / NC) * 64;
+  const size_t smem = (size_t)(prog.n_slots + 1) * kCSlotD * sizeof(double) + (size_t)prog.n_ops * sizeof(ClusterOp);
+  if (smem > 227 * 1024) return -1;
+  cudaError_t e = cudaFuncSetAttribute(plan_cluster_f64_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  plan_cluster_f64_kernel<NC><<<NC, 256, smem, stream>>>(d, A, S, R, prog);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace
 
 int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream) {
   if (d > 64) return -1;
-  const size_t smem = (size_t)(prog.n_slots + 1) * kCSlotD * sizeof(double) + (size_t)prog.n_ops * sizeof(ClusterOp);
-  if (smem > 227 * 1024) return -1;
-  cudaError_t e = cudaFuncSetAttribute(plan_cluster_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  plan_cluster_f64_kernel<<<kClusterCtas, 256, smem, static_cast<cudaStream_t>(stream)>>>(d, A, S, R, prog);
-  return (int)cudaGetLastError();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  static const int nc = std::getenv("NSERIES_SMALL_CLUSTER") ? std::atoi(std::getenv("NSERIES_SMALL_CLUSTER")) : kClusterCtas;
+  if (nc == 2) return launch_cluster_nc<2>(d, prog, A, S, R, s);
+  if (nc == 8) return launch_cluster_nc<8>(d, prog, A, S, R, s);
+  return launch_cluster_nc<4>(d, prog, A, S, R, s);
 }
 
 }  // namespace nseries
