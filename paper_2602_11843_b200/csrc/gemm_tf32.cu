@@ -63,8 +63,12 @@ constexpr int kPrefetchKB = NSERIES_TF32_PREFETCH;   // L2 prefetch distance (k-
 constexpr int KSC = NSERIES_TF32_KSC;        // k-steps (of 8) per accumulation chunk (Kc = 8 KSC)
 constexpr int CPS = (BK / 8) / KSC;          // chunks per smem stage
 constexpr int NBUF = 512 / BN;               // TMEM chunk accumulators of BN columns
-constexpr int kEpiWarps = 8;                 // 2 warps per TMEM lane quarter, BN/2 columns each
-constexpr int EC = BN / 2;                   // columns per epilogue thread
+#ifndef NSERIES_TF32_EPI_WARPS
+#define NSERIES_TF32_EPI_WARPS 8   // (16: 11% slower -- the single MMA-issue thread competes with 20 warps)
+#endif
+constexpr int kEpiWarps = NSERIES_TF32_EPI_WARPS;   // 8: 2 per TMEM lane quarter; 16: 4 per quarter
+constexpr int NG = kEpiWarps / 4;            // column groups of the tile (one per warp of a quarter)
+constexpr int EC = BN / NG;                  // columns per epilogue thread
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 constexpr int kFinalWarps = kThreads / 32;    // every warp runs the final epilogue passes
 constexpr uint32_t kATileBytes = BM * BK * 4;   // 8 KB  (128 rows x 16 k)
@@ -80,14 +84,14 @@ struct Smem {
   alignas(1024) uint8_t xl[STAGES][kATileBytes];
   alignas(1024) uint8_t yh[STAGES][kBTileBytes];
   alignas(1024) uint8_t yl[STAGES][kBTileBytes];
-  uint8_t epi_extra[8192];   // the epilogue staging (3 x [128][EC+1] fp32) spills past the ring
+  uint8_t epi_extra[8192];   // the epilogue staging ((NG+1) x [128][EC+1] fp32) spills past the ring
   alignas(8) uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tmem_full[NBUF];
   uint64_t tmem_empty[NBUF];
   uint32_t tmem_base;
 };
-static_assert(3 * BM * kStageLd * 4 <= STAGES * kStageBytes + 8192, "epilogue staging must fit the TMA ring + epi_extra");
+static_assert((NG + 1) * BM * kStageLd * 4 <= STAGES * kStageBytes + 8192, "epilogue staging must fit the TMA ring + epi_extra");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -277,7 +281,7 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
   // LDS / STS (a generic pointer passed in would not)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* const tiles = reinterpret_cast<float*>(smem_raw + tiles_off);
-  float* const vt = tiles + 2 * BM * kStageLd;   // output values of the current output
+  float* const vt = tiles + NG * BM * kStageLd;   // output values of the current output
   const int n_aux = ep.n_aux, ldp = ep.ldp;
   constexpr int n_out = NO;
   const float* auxb[kMaxAux];
@@ -287,8 +291,8 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
     auxb[x] = x < n_aux ? ep.aux[x] : nullptr;
     auxld[x] = x < n_aux ? ep.aux_ld[x] : 0;
   }
-  for (int hh = 0; hh < 2; ++hh) {
-    const int hn0 = n0 + hh * EC;            // global column of this half
+  for (int hh = 0; hh < NG; ++hh) {
+    const int hn0 = n0 + hh * EC;            // global column of this column group
     float* const tile = tiles + hh * BM * kStageLd;
     asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
 #ifdef NSERIES_TF32_DEBUG
@@ -593,7 +597,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   } else if (warp >= 4) {
     // ---------------- epilogue: drain chunks into fp32 registers, then the fused outputs
     const int q = warp & 3;                    // TMEM lane quarter (hardware: warp % 4)
-    const int half = (warp - 4) >> 2;          // this warp's column half of the tile
+    const int half = (warp - 4) >> 2;          // this warp's column group of the tile
     const int cb = half * EC;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     float acc[EC];
@@ -605,7 +609,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       fence_after();
       const uint32_t t_acc = tmem + lane_off + b * BN + cb;
 #ifndef NSERIES_TF32_NO_DRAIN
-#if NSERIES_TF32_BN == 256
+#if NSERIES_TF32_BN == 256 && NSERIES_TF32_EPI_WARPS == 8
 #pragma unroll
       for (int j = 0; j < EC / 32; j += 2) {   // two 32-column loads in flight
         uint32_t v[32], w[32];
@@ -660,7 +664,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     const long long td = 0;
 #endif
     const uint32_t tiles_off = (uint32_t)(reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw);
-    const int ew = warp >= 4 ? warp - 4 : warp + kEpiWarps;   // 0..11
+    const int ew = warp >= 4 ? warp - 4 : warp + kEpiWarps;   // 0 .. kFinalWarps-1
     if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
     else if (ep.n_out == 2) tile_epilogue<2>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
     else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
