@@ -183,6 +183,25 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
+// Warp-converged issue: every lane of the MMA warp runs the loop (so descriptors and TMEM
+// addresses stay warp-uniform and live in uniform registers) and one elected lane issues.
+__device__ __forceinline__ void mma_tf32_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+               " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+               " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+                   saddr(bar)), "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -509,11 +528,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one thread)
-    if (lane == 0) {
+    // ---------------- MMA issuer: the whole warp runs the loop, one elected lane issues
+    {
 #ifdef NSERIES_TF32_DEBUG
       long long tstart = clock64();
-      if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
+      if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
 #endif
       // The tensor pipe queues only a couple of MMAs, so a blocking barrier wait between two
       // chunks drains it (tools/tcgen05_rate.cu: 97 clk per N=128 MMA in a producer/consumer
@@ -532,7 +551,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
           mbar_wait(&sm.full[s], r & 1);
 #ifdef NSERIES_TF32_DEBUG
-          if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
+          if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
 #endif
         }
         if (u > 0 && !tm_ok) {
@@ -541,7 +560,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
           mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
 #ifdef NSERIES_TF32_DEBUG
-          if (g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
+          if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
 #endif
         }
         fence_after();
@@ -558,24 +577,24 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #pragma unroll
         for (int j = 0; j < KSC; ++j) {
           const int ks = h * KSC + j;
-          mma_tf32(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
-          mma_tf32(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
+          mma_tf32_w(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
+          mma_tf32_w(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
         }
 #pragma unroll
         for (int j = 0; j < KSC; ++j) {
           const int ks = h * KSC + j;
-          mma_tf32(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
+          mma_tf32_w(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
         }
-        mma_commit(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
+        mma_commit_w(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
         if (h == CPS - 1) {
           // frees the smem stage (in every CTA of the cluster: the pair multicasts into it)
           // once these MMAs finish
-          if (CL > 1) mma_commit_mc(&sm.empty[s], (1u << CL) - 1);
-          else mma_commit(&sm.empty[s]);
+          if (CL > 1) mma_commit_mc_w(&sm.empty[s], (1u << CL) - 1);
+          else mma_commit_w(&sm.empty[s]);
         }
       }
 #ifdef NSERIES_TF32_DEBUG
-      if (g_dbg) {
+      if (g_dbg && lane == 0) {
         atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 2, 1ull);
         atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 3, (unsigned long long)(clock64() - tstart));
       }
