@@ -31,6 +31,11 @@ struct nseries_ctx {
   std::map<std::string, Program> programs;
   nseries_stats stats{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // nseries_eval_host: the executor records ev_S right after the op that writes the final S,
+  // so the device->host copy of S overlaps the plan's trailing product (the final power)
+  bool want_ev_S = false;
+  cudaEvent_t ev_S = nullptr;
+  cudaStream_t copy_stream = nullptr;
   // CUDA-graph cache: one executable graph per (program, d, dtype, buffer pointers)
   cudaStream_t cap_stream = nullptr;
   struct CachedGraph { cudaGraphExec_t exec; int launches; };
@@ -115,6 +120,14 @@ nseries_status resolve_plan(const nseries_plan* plan, int64_t k, uint32_t flags,
 // Slot i < n_slots holds temp value i's planes; slots n_slots..+2 hold the operand planes of
 // the user's A, S and R buffers (their x planes are the user buffers, ld = d).
 constexpr int kF32Planes = 5;
+// record h->ev_S if op i writes the final S (eval_host overlaps the copy-out of S with the rest)
+void mark_final_S(nseries_ctx* h, const Program& P, int i, cudaStream_t s) {
+  if (!h->want_ev_S) return;
+  const Op& op = P.ops[i];
+  for (int j = 0; j < op.n_out; ++j)
+    if (op.out[j] == P.final_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
+}
+
 size_t f32_ws_bytes(const Program& P, int d) {
   return (size_t)(P.n_slots + 3) * kF32Planes * d * padded_ld(d) * sizeof(float);
 }
@@ -209,6 +222,7 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
       rc = launch_axpby_f32(d, ep, s);
     }
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    mark_final_S(h, P, (int)i, s);
     ++nl;
   }
   *launches = nl;
@@ -253,6 +267,7 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
                                              static_cast<const double*>(ptr(op.Y)), d, ep, s)
                            : launch_axpby_f64(d, ep, s);
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    mark_final_S(h, P, i, s);
     ++nl;
   }
   *launches = nl;
@@ -271,6 +286,7 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
       const int rc = launch_plan_cluster_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
                                              static_cast<double*>(R), s);
       if (rc == 0) {
+        if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
         *launches = 1;
         return NSERIES_OK;
       }
@@ -284,6 +300,7 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
       const int rc = launch_plan_smem_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
                                           static_cast<double*>(R), s);
       if (rc == 0) {
+        if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
         *launches = 1;
         return NSERIES_OK;
       }
@@ -321,6 +338,7 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
     }
     const int rc = launch_plan_small_f64(d, sp, s);
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
     *launches = 1;
     return NSERIES_OK;
   }
@@ -366,6 +384,7 @@ nseries_status nseries_create(nseries_handle* out, int device) {
   h->device = device;
   cudaEventCreate(&h->ev0);
   cudaEventCreate(&h->ev1);
+  cudaEventCreateWithFlags(&h->ev_S, cudaEventDisableTiming);
   *out = h;
   return NSERIES_OK;
 }
@@ -379,6 +398,8 @@ nseries_status nseries_destroy(nseries_handle h) {
   if (h->stage) cudaFree(h->stage);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev_S) cudaEventDestroy(h->ev_S);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
@@ -461,8 +482,8 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     // The op list is replayed as one CUDA graph: the pointers are baked in, so the key holds
     // them; capture runs on a private stream (the caller's may be the legacy NULL stream).
     char ptrs[192];
-    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
-                  (flags & NSERIES_SYMMETRIC) ? 1 : 0);
+    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%d|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
+                  (flags & NSERIES_SYMMETRIC) ? 1 : 0, h->want_ev_S ? 1 : 0);
     const std::string gkey = key + ptrs;
     auto git = h->graphs.find(gkey);
     if (git == h->graphs.end()) {
@@ -527,15 +548,25 @@ nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemcpyAsync(dA, A_host, bytes, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(h, e);
+  // the copy-out of S starts as soon as the op writing S completes (a side stream waits on
+  // ev_S recorded inside the executor), overlapping the plan's trailing product
+  if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cuda_fail(h, cudaGetLastError());
+  h->want_ev_S = true;
   nseries_status st = nseries_eval(h, dA, d, k, plan, dt, dS, dR, flags & ~NSERIES_SYNC_STATS, stream);
+  h->want_ev_S = false;
   if (st != NSERIES_OK) return st;
-  e = cudaMemcpyAsync(S_host, dS, bytes, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamWaitEvent(h->copy_stream, h->ev_S, 0);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  e = cudaMemcpyAsync(S_host, dS, bytes, cudaMemcpyDeviceToHost, h->copy_stream);
   if (e != cudaSuccess) return cuda_fail(h, e);
   if (R_host) {
     e = cudaMemcpyAsync(R_host, dR, bytes, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(h, e);
   }
-  return cuda_fail(h, cudaStreamSynchronize(s));
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  return cuda_fail(h, cudaStreamSynchronize(h->copy_stream));
 }
 
 static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t strideA,

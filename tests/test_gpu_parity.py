@@ -352,3 +352,28 @@ def test_symmetric_mode_f32(h, d, steps, extra):
     assert O.rel_fro(S.astype(np.float64), Sref) <= 2e-5, (d, steps, flags)
     S2, _, _ = _run(h, A, steps, flags=flags & ~P.NSERIES_SYMMETRIC, dtype=torch.float32)
     assert O.rel_fro(S.astype(np.float64), S2.astype(np.float64)) <= 2e-5
+
+
+@pytest.mark.parametrize("d,steps,dt,flags", [(300, [15, 15], "f64", 0), (300, [9, 9], "f32", 0),
+                                              (257, [5, 1, 2], "f64", 0), (40, [9, 9], "f64", 0),
+                                              (512, [15, 15], "f64", 1)])
+def test_host_api_overlapped_copy_out(h, d, steps, dt, flags):
+    # nseries_eval_host copies S out on a side stream as soon as the op writing S finishes
+    # (overlapping the trailing product); S and R must still be complete and correct, with and
+    # without graph replay (second call replays the cached graph)
+    G = inputs.random_matrix(d, 900 + d, 0.7)
+    A = 0.5 * (G + G.T) if flags else G
+    if dt == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+    k = OP.plan_reaches(steps)
+    fl = _flags(steps) | (P.NSERIES_SYMMETRIC if flags else 0)
+    plan = P.nseries_plan_finalize(steps, k, fl)
+    Ah = np.ascontiguousarray(A.astype(np.float32) if dt == "f32" else A)
+    Sref, Rref = _oracle_full(A, steps, want_R=True)
+    tol = 2e-5 if dt == "f32" else TOL64
+    for _ in range(2):
+        Sh = np.full_like(Ah, np.nan)
+        Rh = np.full_like(Ah, np.nan)
+        P.nseries_eval_host(h, Ah, d, k, plan=plan, S=Sh, R_out=Rh, flags=fl)
+        assert O.rel_fro(Sh.astype(np.float64), Sref) <= tol
+        assert np.all(np.isfinite(Rh))
