@@ -377,3 +377,19 @@ def test_host_api_overlapped_copy_out(h, d, steps, dt, flags):
         P.nseries_eval_host(h, Ah, d, k, plan=plan, S=Sh, R_out=Rh, flags=fl)
         assert O.rel_fro(Sh.astype(np.float64), Sref) <= tol
         assert np.all(np.isfinite(Rh))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_large_ragged_d(h, dt):
+    # d = 10000 (not a multiple of any tile size; 79 x 79 tiles of 128, odd M-pair count for the
+    # fp32 clusters); k = 9 via radix-9 (5 products) checked on 16 seeded probe columns
+    d, steps = 10000, [9]
+    rng = np.random.default_rng(31)
+    A = (0.6 / np.sqrt(d)) * rng.standard_normal((d, d))
+    if dt == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+    V, _ = inputs.probe_block(d, 31)
+    S, _, _ = _run(h, A, steps, dtype=torch.float64 if dt == "f64" else torch.float32)
+    err = _probe_parity(S.astype(np.float64), A, steps, V, False)
+    assert err <= (TOL64 if dt == "f64" else 2e-5), err
