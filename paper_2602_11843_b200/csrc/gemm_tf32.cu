@@ -49,6 +49,13 @@ namespace {
 #endif
 constexpr int BM = 128, BN = NSERIES_TF32_BN, BK = NSERIES_TF32_BK, STAGES = NSERIES_TF32_STAGES;
 constexpr int CL = NSERIES_TF32_CLUSTER;     // 1 or 2 CTAs per cluster
+#ifndef NSERIES_TF32_2SM
+#define NSERIES_TF32_2SM 0   // (correct, but 1.8x slower: the leader waits for both CTAs' drains every chunk)
+#endif
+// 2-SM UMMA: the CTA pair issues ONE tcgen05.mma.cta_group::2 (M = 256) per k-step from the
+// leader CTA; each CTA holds its 128 A rows and its 128-row half of the B tile (no multicast)
+constexpr bool TWO_SM = NSERIES_TF32_2SM != 0;
+static_assert(!TWO_SM || CL == 2, "2-SM UMMA needs CTA pairs");
 #ifndef NSERIES_TF32_PREFETCH
 #define NSERIES_TF32_PREFETCH 0   // (8 measured 19% slower at d = 4096: extra L2 traffic)
 #endif
@@ -201,6 +208,36 @@ __device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
                " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
                    saddr(bar)), "h"(mask)
                : "memory");
+}
+// M = 256 across the CTA pair (leader issues; A rows and B half read from both CTAs' smem)
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+__device__ __forceinline__ void mma2_tf32_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc2), "r"(acc));
+}
+__device__ __forceinline__ void mma2_commit_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+               " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+                   saddr(bar)), "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// TMA whose complete_tx is delivered to the mbarrier at shared::cluster address bar (the leader's)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
@@ -480,15 +517,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CL); }
-    for (int b = 0; b < NBUF; ++b) { mbar_init(&sm.tmem_full[b], 1); mbar_init(&sm.tmem_empty[b], kEpiWarps); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], TWO_SM ? 1 : CL); }
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&sm.tmem_full[b], 1);
+      mbar_init(&sm.tmem_empty[b], TWO_SM ? 2 * kEpiWarps : kEpiWarps);   // 2-SM: both CTAs' drains
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     saddr(&sm.tmem_base)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if constexpr (TWO_SM) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       saddr(&sm.tmem_base)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       saddr(&sm.tmem_base)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   fence_before();
   if (CL > 1) cluster_sync_all();   // the peer's barriers are initialised before any multicast
@@ -505,6 +552,18 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #ifdef NSERIES_TF32_NO_TMA
         mbar_arrive(&sm.full[s]);
 #else
+        if constexpr (TWO_SM) {
+          // both CTAs load their A rows and B half to the same offsets of their own smem; the
+          // bytes are accounted on the LEADER's full barrier (2 x own bytes)
+          const int k0 = kb * BK;
+          const uint32_t fb = mapa_rank(saddr(&sm.full[s]), 0);
+          if (rank == 0) mbar_expect_tx(&sm.full[s], 2 * (2 * kATileBytes + kBTileBytes));
+          tma_load_2d_2sm(sm.xh[s], &mXh, fb, k0, m0);
+          tma_load_2d_2sm(sm.xl[s], &mXl, fb, k0, m0);
+          tma_load_2d_2sm(sm.yh[s], &mYh, fb, k0, n0 + rank * (BN / 2));
+          tma_load_2d_2sm(sm.yl[s], &mYl, fb, k0, n0 + rank * (BN / 2));
+          continue;
+        }
         mbar_expect_tx(&sm.full[s], kStageBytes);
         const int k0 = kb * BK;
         tma_load_2d(sm.xh[s], &mXh, &sm.full[s], k0, m0);
@@ -529,7 +588,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: the whole warp runs the loop, one elected lane issues
-    {
+    // (2-SM UMMA: only the leader CTA issues, for both CTAs of the pair)
+    if (!TWO_SM || rank == 0) {
 #ifdef NSERIES_TF32_DEBUG
       long long tstart = clock64();
       if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
@@ -574,23 +634,39 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         const uint32_t t_acc = tmem + b * BN;
         // small cross terms first (accumulator still small), hi*hi last; K-major swizzled
         // tiles advance 32 B (8 tf32, +2 in the >>4 address field) per k-step
+        if constexpr (TWO_SM) {
 #pragma unroll
-        for (int j = 0; j < KSC; ++j) {
-          const int ks = h * KSC + j;
-          mma_tf32_w(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
-          mma_tf32_w(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
-        }
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma2_tf32_w(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
+            mma2_tf32_w(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
+          }
 #pragma unroll
-        for (int j = 0; j < KSC; ++j) {
-          const int ks = h * KSC + j;
-          mma_tf32_w(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
-        }
-        mma_commit_w(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
-        if (h == CPS - 1) {
-          // frees the smem stage (in every CTA of the cluster: the pair multicasts into it)
-          // once these MMAs finish
-          if (CL > 1) mma_commit_mc_w(&sm.empty[s], (1u << CL) - 1);
-          else mma_commit_w(&sm.empty[s]);
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma2_tf32_w(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
+          }
+          mma2_commit_mc_w(&sm.tmem_full[b], 3);   // both CTAs' accumulators ready
+          if (h == CPS - 1) mma2_commit_mc_w(&sm.empty[s], 3);
+        } else {
+#pragma unroll
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma_tf32_w(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
+            mma_tf32_w(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
+          }
+#pragma unroll
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma_tf32_w(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
+          }
+          mma_commit_w(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
+          if (h == CPS - 1) {
+            // frees the smem stage (in every CTA of the cluster: the pair multicasts into it)
+            // once these MMAs finish
+            if (CL > 1) mma_commit_mc_w(&sm.empty[s], (1u << CL) - 1);
+            else mma_commit_w(&sm.empty[s]);
+          }
         }
       }
 #ifdef NSERIES_TF32_DEBUG
@@ -657,7 +733,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
 #endif
       fence_before();
-      if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
+      if (lane == 0) {
+        if constexpr (TWO_SM) mbar_arrive_cluster(mapa_rank(saddr(&sm.tmem_empty[b]), 0));   // leader's
+        else mbar_arrive(&sm.tmem_empty[b]);
+      }
     }
 #ifdef NSERIES_TF32_DEBUG
     t_drained = clock64();
@@ -699,7 +778,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   else __syncthreads();
   if (warp == 2) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+    if constexpr (TWO_SM) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
