@@ -282,7 +282,7 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
   if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode == 0) {
     // 4-CTA cluster, each CTA a 16-row block of every value (DSMEM for the operand rows)
     WarpProgram wp{};
-    if (build_warp_program(P, &wp, /*inplace=*/false) == NSERIES_OK) {
+    if (build_cluster_program(P, &wp) == NSERIES_OK) {
       const int rc = launch_plan_cluster_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
                                              static_cast<double*>(R), s);
       if (rc == 0) {

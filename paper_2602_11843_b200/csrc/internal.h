@@ -111,6 +111,7 @@ int launch_batched(nseries_dtype dt, const void* A, int64_t strideA, const void*
 // shared-memory slot, kWSlotA the current A_b buffer, kWSlotI the identity (synthesised in
 // fragment registers, operands only), kWSlotNone (output not kept in shared memory).
 constexpr int kWSlotNone = -1, kWSlotA = -2, kWSlotI = -3;
+constexpr int kWSlotRep = 64;   // cluster kernel: code kWSlotRep + i = replicated slot i
 struct WarpOp {
   int8_t gemm, X, Y, n_aux, n_out, gmask;   // gmask bit j: output j is the final S (global)
   int8_t rmask;                             // rmask bit j: output j is the final R (global)
@@ -125,6 +126,7 @@ struct WarpOp {
 struct WarpProgram {
   int n_ops, n_slots;
   unsigned probe_delay_ns;         // harness-only experiments (tools/bw_probe.cu); 0 in the library
+  int n_rep;                       // cluster kernel: slots replicated in every CTA (codes >= kWSlotRep)
   WarpOp ops[kMaxBatchedOps];
 };
 // Map a compiled op list onto the warp kernel's slot codes (in-place slot assignment; the final
@@ -185,6 +187,10 @@ int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double
 // Cluster of 4 CTAs, each holding a 16-row block of every value (operand rows of the other CTAs
 // read through distributed shared memory); prog built with inplace = false.  -1 if unsupported.
 int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
+// Slot layout for the cluster kernel: values read as a right operand live in slots replicated in
+// every CTA (each CTA pushes its rows of such outputs to all peers); the others in per-CTA
+// row-block slots.  No in-place reuse.
+nseries_status build_cluster_program(const Program& P, WarpProgram* wp);
 
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "internal.h"
 
@@ -277,55 +278,75 @@ struct __align__(16) ClusterOp {
   double alpha[kMaxOut], beta[kMaxOut][kMaxAux], gamma[kMaxOut];
   int x, y, kind, n_aux, n_out, gmask, rmask, pad;   // kind: 0 axpby, 1 gemm, 2 X = I, 3 Y = I
   int aux[kMaxAux], out[kMaxOut];                      // offsets (doubles); out < 0: not kept
+  int push, pad2[3];                                   // bit q: output q is replicated (pushed)
 };
 
 template <int NC>   // CTAs per cluster; each owns RPC = 64 / NC rows of every value
 __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(256, 1)
 plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict__ S, double* __restrict__ R,
                         const __grid_constant__ WarpProgram prog) {
-  constexpr int RPC = 64 / NC, MB = RPC / 8, kCSlotD = RPC * 64;
+  constexpr int RPC = 64 / NC, MB = RPC / 8, kLSlotD = RPC * 64, kRSlotD = 64 * 64;
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double smc[];
   const int rank = (int)cluster.block_rank();
   const int r0 = rank * RPC;
   const int n_ops = prog.n_ops;
-  double* const sA = smc + prog.n_slots * kCSlotD;
-  ClusterOp* const sops = reinterpret_cast<ClusterOp*>(smc + (prog.n_slots + 1) * kCSlotD);
-  const double* peer[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) peer[c] = cluster.map_shared_rank(smc, c);
+  // layout: [row-block slots: n_slots x RPC x 64] [replicated slots: n_rep x 64 x 64] [A: 64 x 64]
+  const int rep_base = prog.n_slots * kLSlotD;
+  const int a_base = rep_base + prog.n_rep * kRSlotD;
+  ClusterOp* const sops = reinterpret_cast<ClusterOp*>(smc + a_base + kRSlotD);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wn0 = warp * 8;            // 8 warps x 8 output columns; each warp all 16 local rows
-  auto off_of = [&](int code) -> int { return code == kWSlotA ? prog.n_slots * kCSlotD : (code > 0 ? code : 0) * kCSlotD; };
+  const int wn0 = warp * 8;            // 8 warps x 8 output columns; each warp all local rows
+  // own-row base of a value (row-block slot, or this CTA's rows inside a replicated slot / A)
+  auto own_of = [&](int code) -> int {
+    if (code == kWSlotA) return a_base + r0 * 64;
+    if (code >= kWSlotRep) return rep_base + (code - kWSlotRep) * kRSlotD + r0 * 64;
+    return (code > 0 ? code : 0) * kLSlotD;
+  };
+  // full (all 64 rows) base of a replicated value (right operands)
+  auto full_of = [&](int code) -> int {
+    if (code == kWSlotA) return a_base;
+    return rep_base + (code >= kWSlotRep ? code - kWSlotRep : 0) * kRSlotD;
+  };
   for (int i = tid; i < n_ops; i += 256) {
     const WarpOp& w = prog.ops[i];
     ClusterOp c;
     c.kind = !w.gemm ? 0 : (w.X == kWSlotI ? 2 : (w.Y == kWSlotI ? 3 : 1));
-    c.x = off_of(w.X);
-    c.y = off_of(w.Y);
+    c.x = own_of(w.X);
+    c.y = full_of(w.Y);
     c.n_aux = w.n_aux;
     c.n_out = w.n_out;
     c.gmask = w.gmask;
     c.rmask = w.rmask;
     c.pad = 0;
-    for (int x = 0; x < kMaxAux; ++x) c.aux[x] = off_of(x < w.n_aux ? w.aux[x] : 0);
+    for (int x = 0; x < kMaxAux; ++x) c.aux[x] = own_of(x < w.n_aux ? w.aux[x] : 0);
+    c.push = 0;
     for (int q = 0; q < kMaxOut; ++q) {
-      c.out[q] = (q < w.n_out && w.out[q] >= 0) ? w.out[q] * kCSlotD : -1;
+      const bool keep = q < w.n_out && w.out[q] != kWSlotNone;
+      c.out[q] = keep ? own_of(w.out[q]) : -1;
+      if (keep && w.out[q] >= kWSlotRep) c.push |= 1 << q;
       c.alpha[q] = w.dalpha[q];
       c.gamma[q] = w.dgamma[q];
       for (int x = 0; x < kMaxAux; ++x) c.beta[q][x] = w.dbeta[q][x];
     }
     sops[i] = c;
   }
-  // local row block of A (zero padded)
-  for (int i = tid; i < kCSlotD; i += 256) {
-    const int rl = i >> 6, c = i & 63, r = r0 + rl;
+  // A: every CTA holds all 64 rows (A is read as a right operand), zero padded
+  for (int i = tid; i < kRSlotD; i += 256) {
+    const int r = i >> 6, c = i & 63;
     const bool ok = r < d && c < d;
-    cp8(sA + swz64(rl, c), ok ? A + (size_t)r * d + c : A, ok);
+    cp8(smc + a_base + swz64(r, c), ok ? A + (size_t)r * d + c : A, ok);
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  // shared::cluster address of this CTA's slot area in every peer (pushes go to the same offset)
+  uint32_t peer[NC];
+  {
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smc));
+#pragma unroll
+    for (int c = 0; c < NC; ++c) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer[c]) : "r"(base), "r"(c));
+  }
   cluster.sync();
 #ifdef NSERIES_SMALL_PROFILE
   long long tp0 = clock64();
@@ -333,8 +354,7 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #endif
   for (int o = 0; o < n_ops; ++o) {
     const ClusterOp& op = sops[o];
-    // KS independent partial accumulators per row block (k-steps s with s % KS == p) keep KS
-    // DMMA chains in flight per row block instead of one 16-long dependent chain
+    // KS independent partial accumulators per row block (k-steps s with s % KS == p)
     constexpr int KS = 4;
     double part[MB][KS][2];
 #pragma unroll
@@ -345,23 +365,17 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     if (kind != 0) {
       const bool xi = kind == 2, yi = kind == 3;
       const int xo = op.x, yo = op.y;
-      // B fragments: Y[k + t][wn0 + g] for the 16 k-steps, rows owned by CTA (k + t) / RPC;
-      // all issued before the first MMA (remote latency)
-      double bf[16];
       const int col = wn0 + g;
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const int k = 4 * s + t;
-        bf[s] = yi ? ((k == col && col < d) ? 1.0 : 0.0) : peer[k / RPC][yo + swz64(k % RPC, col)];
-      }
-#pragma unroll
-      for (int s = 0; s < 16; ++s) {
-        const int k = 4 * s + t;
+        // right operand: the local replica holds all 64 rows
+        const double b = yi ? ((k == col && col < d) ? 1.0 : 0.0) : smc[yo + swz64(k, col)];
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
           const int rl = i * 8 + g;
           const double a = xi ? ((r0 + rl == k && r0 + rl < d) ? 1.0 : 0.0) : smc[xo + swz64(rl, k)];
-          dmma884(part[i][s % KS], a, bf[s]);
+          dmma884(part[i][s % KS], a, b);
         }
       }
     }
@@ -373,7 +387,9 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #ifdef NSERIES_SMALL_PROFILE
     if (tid == 0 && rank == 0) g_small_prof[1 + 3 * o] = clock64() + (long long)(acc[0][0] * 0.0);
 #endif
-    // epilogue on local rows (no barrier needed before it: outputs never alias this op's operands)
+    // epilogue on local rows; outputs read later as right operands are pushed to every peer's
+    // replica (same offset) -- no barrier needed before it: outputs never alias this op's
+    // operands (slots are not reused in place)
     const int n_aux = op.n_aux, n_out = op.n_out;
 #pragma unroll
     for (int i = 0; i < MB; ++i) {
@@ -395,7 +411,17 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
         }
         if (row == colp && row < d) v0 += op.gamma[q];
         if (row == colp + 1 && row < d) v1 += op.gamma[q];
-        if (op.out[q] >= 0) *reinterpret_cast<double2*>(smc + op.out[q] + off) = make_double2(v0, v1);
+        if (op.out[q] >= 0) {
+          *reinterpret_cast<double2*>(smc + op.out[q] + off) = make_double2(v0, v1);
+          if (op.push & (1 << q)) {
+            const uint32_t lo = 8u * (uint32_t)(op.out[q] + off);
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+              if (c != rank)
+                asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(peer[c] + lo), "d"(v0), "d"(v1)
+                             : "memory");
+          }
+        }
         double* gdst = (op.gmask & (1 << q)) ? S : ((op.rmask & (1 << q)) ? R : nullptr);
         if (gdst && row < d) {
           if (colp < d) gdst[(size_t)row * d + colp] = v0;
@@ -406,7 +432,7 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #ifdef NSERIES_SMALL_PROFILE
     if (tid == 0 && rank == 0) g_small_prof[2 + 3 * o] = clock64();
 #endif
-    cluster.sync();   // this op's rows are visible to every CTA before the next op reads them
+    cluster.sync();   // every pushed row is visible cluster-wide before the next op reads it
 #ifdef NSERIES_SMALL_PROFILE
     if (tid == 0 && rank == 0) g_small_prof[3 + 3 * o] = clock64();
 #endif
@@ -415,8 +441,9 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 
 template <int NC>
 int launch_cluster_nc(int d, const WarpProgram& prog, const double* A, double* S, double* R, cudaStream_t stream) {
-  constexpr int kCSlotD = (64 / NC) * 64;
-  const size_t smem = (size_t)(prog.n_slots + 1) * kCSlotD * sizeof(double) + (size_t)prog.n_ops * sizeof(ClusterOp);
+  constexpr int kLSlotD = (64 / NC) * 64;
+  const size_t smem = ((size_t)prog.n_slots * kLSlotD + (size_t)(prog.n_rep + 1) * 4096) * sizeof(double) +
+                      (size_t)prog.n_ops * sizeof(ClusterOp);
   if (smem > 227 * 1024) return -1;
   cudaError_t e = cudaFuncSetAttribute(plan_cluster_f64_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
@@ -426,13 +453,82 @@ int launch_cluster_nc(int d, const WarpProgram& prog, const double* A, double* S
 
 }  // namespace
 
+nseries_status build_cluster_program(const Program& P, WarpProgram* out) {
+  if ((int)P.ops.size() > kMaxBatchedOps) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  const int nv = P.n_values;
+  std::vector<int> last_use(nv, -1), producer(nv, -1);
+  std::vector<char> rep(nv, 0);
+  for (int i = 0; i < (int)P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    if (op.gemm) { last_use[op.X] = i; last_use[op.Y] = i; rep[op.Y] = 1; }
+    for (int a = 0; a < op.n_aux; ++a) last_use[op.aux[a]] = i;
+    for (int j = 0; j < op.n_out; ++j) producer[op.out[j]] = i;
+  }
+  auto needs_slot = [&](int v) {
+    return P.val_kind[v] == V_TEMP || ((v == P.final_S || v == P.final_R) && last_use[v] >= 0);
+  };
+  // two pools, slots freed after the outputs of the op reading them last are placed
+  std::vector<int> slot(nv, -1);
+  std::vector<int> free_l, free_r;
+  int n_l = 0, n_r = 0;
+  for (int i = 0; i < (int)P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    for (int j = 0; j < op.n_out; ++j) {
+      const int v = op.out[j];
+      if (!needs_slot(v)) continue;
+      std::vector<int>& fl = rep[v] ? free_r : free_l;
+      int sidx;
+      if (!fl.empty()) { sidx = fl.back(); fl.pop_back(); }
+      else sidx = rep[v] ? n_r++ : n_l++;
+      slot[v] = sidx;
+    }
+    for (int v = 0; v < nv; ++v)
+      if (slot[v] >= 0 && ((last_use[v] == i && producer[v] < i) || (producer[v] == i && last_use[v] < 0)))
+        (rep[v] ? free_r : free_l).push_back(slot[v]);
+  }
+  if (n_l >= kWSlotRep || n_r > 127 - kWSlotRep) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  WarpProgram& wp = *out;
+  wp = WarpProgram{};
+  wp.n_slots = n_l;
+  wp.n_rep = n_r;
+  wp.n_ops = (int)P.ops.size();
+  auto code = [&](int v) -> int {
+    if (P.val_kind[v] == V_USER_A) return kWSlotA;
+    if (P.val_kind[v] == V_IDENT) return kWSlotI;
+    if (slot[v] < 0) return kWSlotNone;
+    return rep[v] ? kWSlotRep + slot[v] : slot[v];
+  };
+  for (int i = 0; i < wp.n_ops; ++i) {
+    const Op& op = P.ops[i];
+    WarpOp& w = wp.ops[i];
+    w.gemm = op.gemm ? 1 : 0;
+    w.X = op.gemm ? (int8_t)code(op.X) : 0;
+    w.Y = op.gemm ? (int8_t)code(op.Y) : 0;
+    if (op.gemm && w.X == kWSlotI && w.Y == kWSlotI) return NSERIES_ERR_INVALID_ARG;
+    w.n_aux = (int8_t)op.n_aux;
+    w.n_out = (int8_t)op.n_out;
+    w.gmask = 0;
+    w.rmask = 0;
+    for (int a = 0; a < kMaxAux; ++a) w.aux[a] = a < op.n_aux ? (int8_t)code(op.aux[a]) : 0;
+    for (int j = 0; j < kMaxOut; ++j) {
+      w.out[j] = j < op.n_out ? (int8_t)code(op.out[j]) : kWSlotNone;
+      if (j < op.n_out && op.out[j] == P.final_S) w.gmask |= (int8_t)(1 << j);
+      if (j < op.n_out && op.out[j] == P.final_R) w.rmask |= (int8_t)(1 << j);
+      w.dalpha[j] = op.alpha[j];
+      w.dgamma[j] = op.gamma[j];
+      for (int a = 0; a < kMaxAux; ++a) w.dbeta[j][a] = op.beta[j][a];
+    }
+  }
+  return NSERIES_OK;
+}
+
 int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream) {
   if (d > 64) return -1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   static const int nc = std::getenv("NSERIES_SMALL_CLUSTER") ? std::atoi(std::getenv("NSERIES_SMALL_CLUSTER")) : kClusterCtas;
   if (nc == 2) return launch_cluster_nc<2>(d, prog, A, S, R, s);
-  if (nc == 8) return launch_cluster_nc<8>(d, prog, A, S, R, s);
-  return launch_cluster_nc<4>(d, prog, A, S, R, s);
+  if (nc == 4) return launch_cluster_nc<4>(d, prog, A, S, R, s);
+  return launch_cluster_nc<8>(d, prog, A, S, R, s);
 }
 
 }  // namespace nseries

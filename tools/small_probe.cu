@@ -12,7 +12,7 @@ int main() {
   Program P;
   if (compile_plan(plan, false, &P) != NSERIES_OK) return 1;
   WarpProgram wp;
-  if (build_warp_program(P, &wp, false) != NSERIES_OK) return 1;
+  if (build_cluster_program(P, &wp) != NSERIES_OK) return 1;
   const int d = 64;
   std::vector<double> h(d * d);
   for (int i = 0; i < d * d; ++i) h[i] = ((i * 2654435761u) % 1000) / 1000.0 * 0.02;
@@ -21,7 +21,7 @@ int main() {
   for (int it = 0; it < 5; ++it) launch_plan_cluster_f64(d, wp, A, S, nullptr, 0);
   cudaDeviceSynchronize();
   long long p[256]; cudaMemcpyFromSymbol(p, g_small_prof, sizeof(p));
-  printf("ops %d slots %d (%s)\n", wp.n_ops, wp.n_slots, cudaGetErrorString(cudaGetLastError()));
+  printf("ops %d slots %d rep %d (%s)\n", wp.n_ops, wp.n_slots, wp.n_rep, cudaGetErrorString(cudaGetLastError()));
   long long prev = p[0];
   for (int o = 0; o < wp.n_ops; ++o) {
     printf("op %2d: mainloop %6lld  epilogue %6lld  barrier %6lld cycles\n", o, p[1 + 3 * o] - prev,
