@@ -43,6 +43,9 @@ struct nseries_ctx {
   // small fp64 single-matrix kernels (d <= 64): 0 cluster (default) -> 1 single-CTA shared
   // memory -> 2 single-CTA global slots; NSERIES_SMALL_MODE selects the first one tried
   int small_mode = 0;
+  // fp32 engine split-K workspace (tail-wave partial accumulators + per-tile counters)
+  void* sk_ws = nullptr;
+  size_t sk_bytes = 0;
 };
 
 namespace {
@@ -70,6 +73,25 @@ nseries_status ensure_ws(nseries_ctx* h, size_t bytes) {
     return NSERIES_ERR_OOM;
   }
   h->ws_bytes = bytes;
+  return NSERIES_OK;
+}
+
+// split-K workspace of the fp32 engine at size d (counters zeroed; the kernel re-zeroes them)
+nseries_status ensure_splitk(nseries_ctx* h, int d) {
+  const size_t bytes = tf32_splitk_ws_bytes(d);
+  if (bytes == 0 || bytes <= h->sk_bytes) return NSERIES_OK;
+  if (h->sk_ws) {
+    cudaDeviceSynchronize();
+    cudaFree(h->sk_ws);
+    h->sk_ws = nullptr;
+    h->sk_bytes = 0;
+  }
+  if (cudaMalloc(&h->sk_ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return NSERIES_ERR_OOM;
+  }
+  if (cudaMemset(h->sk_ws, 0, bytes) != cudaSuccess) return cuda_fail(h, cudaGetLastError());
+  h->sk_bytes = bytes;
   return NSERIES_OK;
 }
 
@@ -217,7 +239,7 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
     int rc;
     if (op.gemm) {
       const int l = lr[i].first, r = lr[i].second;
-      rc = launch_gemm_tf32x3(hi(l), lo(l), hiT(r), loT(r), d, ldp, ep, s);
+      rc = launch_gemm_tf32x3(hi(l), lo(l), hiT(r), loT(r), d, ldp, ep, s, h->sk_ws);
     } else {
       rc = launch_axpby_f32(d, ep, s);
     }
@@ -394,6 +416,7 @@ nseries_status nseries_destroy(nseries_handle h) {
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   if (h->ws) cudaFree(h->ws);
+  if (h->sk_ws) cudaFree(h->sk_ws);
   if (h->ident) cudaFree(h->ident);
   if (h->stage) cudaFree(h->stage);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -462,6 +485,7 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   cudaSetDevice(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   st = ensure_ws(h, dt == NSERIES_F64 ? (size_t)P.n_slots * d * d * sizeof(double) : f32_ws_bytes(P, d));
+  if (st == NSERIES_OK && dt == NSERIES_F32) st = ensure_splitk(h, d);
   if (st != NSERIES_OK) return st;
   if (P.needs_identity) {
     st = ensure_identity(h, d, dt, s);
@@ -481,9 +505,9 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   if (!(flags & NSERIES_NO_GRAPH)) {
     // The op list is replayed as one CUDA graph: the pointers are baked in, so the key holds
     // them; capture runs on a private stream (the caller's may be the legacy NULL stream).
-    char ptrs[192];
-    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%d|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
-                  (flags & NSERIES_SYMMETRIC) ? 1 : 0, h->want_ev_S ? 1 : 0);
+    char ptrs[224];
+    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%p|%d|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
+                  h->sk_ws, (flags & NSERIES_SYMMETRIC) ? 1 : 0, h->want_ev_S ? 1 : 0);
     const std::string gkey = key + ptrs;
     auto git = h->graphs.find(gkey);
     if (git == h->graphs.end()) {
@@ -790,6 +814,7 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
     const int ldp = padded_ld(d);
     const size_t plane = (size_t)d * ldp;
     nseries_status st = ensure_ws(h, 4 * plane * sizeof(float));
+    if (st == NSERIES_OK) st = ensure_splitk(h, d);
     if (st != NSERIES_OK) return st;
     float* w = static_cast<float*>(h->ws);
     rc = launch_split_f32(static_cast<const float*>(X), d, w, w + plane, nullptr, nullptr, ldp, d, false, stream);
@@ -803,7 +828,7 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
     e32.out_x[0] = static_cast<float*>(C);
     e32.out_ld[0] = d;
     e32.alpha[0] = 1.f;
-    if (!rc) rc = launch_gemm_tf32x3(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream);
+    if (!rc) rc = launch_gemm_tf32x3(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream, h->sk_ws);
     launches = 3;
   }
   h->stats = nseries_stats{};

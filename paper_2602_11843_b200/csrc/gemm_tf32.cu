@@ -28,6 +28,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <map>
+#include <cstdlib>
 #include <mutex>
 #include <tuple>
 
@@ -97,6 +98,7 @@ struct Smem {
   uint64_t tmem_full[NBUF];
   uint64_t tmem_empty[NBUF];
   uint32_t tmem_base;
+  int sk_last;               // split-K: this CTA finishes the tile (1) or only leaves its partial (0)
 };
 static_assert((NG + 1) * BM * kStageLd * 4 <= STAGES * kStageBytes + 8192, "epilogue staging must fit the TMA ring + epi_extra");
 
@@ -493,7 +495,12 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   // cluster of CL CTAs: same n0, consecutive row tiles; each CTA TMA-loads 1/CL of the B tile
   // and multicasts it to the pair (a CTA whose rows fall past d still runs the protocol)
   const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
-  const int pair = blockIdx.x / CL;
+  // split-K units of the last partial wave: unit u >= sk_first covers K range sp of pair tile
+  // sk_first + (u - sk_first) / sk_split
+  const int unit = blockIdx.x / CL;
+  const bool split = ep.sk_split > 1 && unit >= ep.sk_first;
+  const int pair = split ? ep.sk_first + (unit - ep.sk_first) / ep.sk_split : unit;
+  const int sp = split ? (unit - ep.sk_first) % ep.sk_split : 0;
   int m0, n0;
   bool diag_pair = false;
   if (ep.sym) {
@@ -509,7 +516,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     m0 = ((pair / ntn) * CL + rank) * BM;
     n0 = (pair % ntn) * BN;
   }
-  const int KB = (d + BK - 1) / BK;
+  const int KBt = (d + BK - 1) / BK;
+  const int kb0 = split ? KBt * sp / ep.sk_split : 0;
+  const int KB = split ? KBt * (sp + 1) / ep.sk_split - kb0 : KBt;   // this unit's k-blocks
   const int NC = KB * CPS;                   // accumulation chunks
 #ifdef NSERIES_TF32_DEBUG
   const long long t_kernel0 = clock64();
@@ -555,7 +564,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         if constexpr (TWO_SM) {
           // both CTAs load their A rows and B half to the same offsets of their own smem; the
           // bytes are accounted on the LEADER's full barrier (2 x own bytes)
-          const int k0 = kb * BK;
+          const int k0 = (kb0 + kb) * BK;
           const uint32_t fb = mapa_rank(saddr(&sm.full[s]), 0);
           if (rank == 0) mbar_expect_tx(&sm.full[s], 2 * (2 * kATileBytes + kBTileBytes));
           tma_load_2d_2sm(sm.xh[s], &mXh, fb, k0, m0);
@@ -565,11 +574,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
           continue;
         }
         mbar_expect_tx(&sm.full[s], kStageBytes);
-        const int k0 = kb * BK;
+        const int k0 = (kb0 + kb) * BK;
         tma_load_2d(sm.xh[s], &mXh, &sm.full[s], k0, m0);
         tma_load_2d(sm.xl[s], &mXl, &sm.full[s], k0, m0);
         if (kPrefetchKB > 0 && kb + kPrefetchKB < KB) {   // pull a later k-block into L2 (DRAM latency)
-          const int kp = (kb + kPrefetchKB) * BK;
+          const int kp = (kb0 + kb + kPrefetchKB) * BK;
           tma_prefetch_2d(&mXh, kp, m0);
           tma_prefetch_2d(&mXl, kp, m0);
           tma_prefetch_2d(&mYh, kp, n0 + rank * (BN / CL));
@@ -752,6 +761,49 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     const int rl = q * 32 + lane;
 #pragma unroll
     for (int i = 0; i < EC; ++i) tiles[(half * BM + rl) * kStageLd + i] = acc[i];
+    if (split) {
+      // split-K (2 K ranges): the first CTA of the tile to finish leaves its partial, the
+      // second adds it (p_0 + p_1 is exact-commutative, so the result does not depend on who
+      // finishes first).  Partials are stored as [tile][BN/4][BM][4] floats: a warp's float4
+      // accesses are contiguous.  Works on the staged values (accumulator registers are dead).
+      const int tile = (pair - ep.sk_first) * CL + rank;
+      unsigned* cnt = ep.sk_cnt + 2 * tile;
+      float4* const pt = reinterpret_cast<float4*>(ep.sk_part + (size_t)tile * (BN * BM)) + (size_t)(cb / 4) * BM + rl;
+      float* const st = tiles + (half * BM + rl) * kStageLd;
+      if (warp == 4 && lane == 0) sm.sk_last = atomicAdd(cnt, 1u) == 1u;
+      asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kEpiWarps) : "memory");
+      if (!sm.sk_last) {
+#pragma unroll
+        for (int i = 0; i < EC; i += 4) __stcg(pt + (size_t)(i / 4) * BM, make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]));
+        __threadfence();
+        asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kEpiWarps) : "memory");
+        if (warp == 4 && lane == 0) atomicAdd(cnt + 1, 1u);
+      } else {
+        if (warp == 4 && lane == 0) {
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(cnt + 1) : "memory");
+          } while (v != 1u);
+          cnt[0] = 0u;     // the other unit of this tile is done with the counters
+          cnt[1] = 0u;
+        }
+        asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kEpiWarps) : "memory");
+#pragma unroll
+        for (int i0 = 0; i0 < EC; i0 += 64) {          // 16 independent float4 loads in flight
+          float4 v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = __ldcg(pt + (size_t)((i0 + 4 * u) / 4) * BM);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int i = i0 + 4 * u;
+            st[i] += v[u].x;
+            st[i + 1] += v[u].y;
+            st[i + 2] += v[u].z;
+            st[i + 3] += v[u].w;
+          }
+        }
+      }
+    }
   }
   {
     // ---- final epilogue passes on ALL warps (the producer / MMA / allocator / prefetch warps
@@ -763,7 +815,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
     const uint32_t tiles_off = (uint32_t)(reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw);
     const int ew = warp >= 4 ? warp - 4 : warp + kEpiWarps;   // 0 .. kFinalWarps-1
-    if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
+    if (split) __syncthreads();      // sm.sk_last is visible to every warp
+    if (split && !sm.sk_last) {
+      // partial written: nothing more for this CTA
+    } else if (ep.n_out == 1) tile_epilogue<1>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
     else if (ep.n_out == 2) tile_epilogue<2>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
     else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
   }
@@ -883,10 +938,86 @@ struct MapCache {
 };
 MapCache g_maps;
 
+// concurrently resident clusters of the GEMM kernel (one wave)
+int wave_clusters() {
+  static int w = -1;
+  if (w < 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(148 * CL);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sizeof(Smem) + 1024;
+    cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_tf32x3_kernel, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 0;
+    }
+    w = n;
+  }
+  return w;
+}
+
+// split-K of the tail: with T pair tiles and W resident clusters the last wave holds
+// t = T mod W tiles; each is split into S = min(W / t, kMaxSplit) K ranges when S >= 2
+constexpr int kMaxSplit = 2;            // the combine relies on p_0 + p_1 = p_1 + p_0
+constexpr int kSplitMinKB = 16;            // keep at least 16 k-blocks (K = 256) per unit
+void splitk_plan(int d, bool sym, int* first, int* S) {
+  *first = 0;
+  *S = 1;
+  static const bool off = std::getenv("NSERIES_TF32_SPLITK") && std::atoi(std::getenv("NSERIES_TF32_SPLITK")) == 0;
+  if (sym || off || NSERIES_TF32_2SM) return;
+  const int ntn = (d + BN - 1) / BN;
+  const int T = ((d + BM - 1) / BM + CL - 1) / CL * ntn;
+  const int W = wave_clusters();
+  if (W <= 0) return;
+  const int t = T % W;                     // T < W: a single partial wave, split all of it
+  if (t == 0) return;
+  int s = std::min(W / t, kMaxSplit);
+  while (s > 1 && (d + BK - 1) / BK / s < kSplitMinKB) --s;
+  if (s < 2 || (size_t)t * CL * 2 * sizeof(unsigned) > 8192) return;
+  *first = T - t;
+  *S = s;
+}
+
+// split-K workspace layout: [counters: 2 x unsigned per CTA tile, fixed 8 KiB area][partials].
+// The counter area is at the same place for every d (the partials of one size must never land
+// on counters another size expects to be zero); split tiles < one wave <= 1024 CTA tiles.
+constexpr size_t kSplitCntBytes = 8192;
+size_t splitk_cnt_bytes(size_t) { return kSplitCntBytes; }
+
 }  // namespace
 
+size_t tf32_splitk_ws_bytes(int d) {
+  int first, S;
+  splitk_plan(d, false, &first, &S);
+  if (S < 2) return 0;
+  const int ntn = (d + BN - 1) / BN;
+  const int T = ((d + BM - 1) / BM + CL - 1) / CL * ntn;
+  const size_t tiles = (size_t)(T - first) * CL;
+  return splitk_cnt_bytes(tiles) + tiles * (size_t)(BN * BM) * sizeof(float);
+}
+
 int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
-                       const EpiParamsF32& ep, void* stream) {
+                       const EpiParamsF32& ep_in, void* stream, void* sk_ws) {
+  EpiParamsF32 ep = ep_in;
+  ep.sk_first = 0;
+  ep.sk_split = 1;
+  ep.sk_part = nullptr;
+  ep.sk_cnt = nullptr;
+  if (sk_ws && !ep.sym) {
+    int first, S;
+    splitk_plan(d, false, &first, &S);
+    if (S > 1) {
+      const int ntn = (d + BN - 1) / BN;
+      const int T = ((d + BM - 1) / BM + CL - 1) / CL * ntn;
+      const size_t tiles = (size_t)(T - first) * CL;
+      ep.sk_first = first;
+      ep.sk_split = S;
+      ep.sk_cnt = static_cast<unsigned*>(sk_ws);
+      const size_t off = splitk_cnt_bytes(tiles);
+      ep.sk_part = reinterpret_cast<float*>(static_cast<char*>(sk_ws) + off);
+    }
+  }
   CUtensorMap mxh, mxl, myh, myl;
   int rc = g_maps.get(Xh, d, ldp, 0, &mxh);
   if (!rc) rc = g_maps.get(Xl, d, ldp, 0, &mxl);
@@ -903,7 +1034,8 @@ int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const 
   const int row_groups = ((d + BM - 1) / BM + CL - 1) / CL;   // clusters of CL row tiles
   const int ntn = (d + BN - 1) / BN;
   if (ep.sym && CL * BM != BN) return (int)cudaErrorInvalidValue;   // square pair tiles needed
-  const int ctas = ep.sym ? ntn * (ntn + 1) / 2 * CL : row_groups * ntn * CL;
+  int ctas = ep.sym ? ntn * (ntn + 1) / 2 * CL : row_groups * ntn * CL;
+  if (ep.sk_split > 1) ctas += (row_groups * ntn - ep.sk_first) * (ep.sk_split - 1) * CL;
   gemm_tf32x3_kernel<<<ctas, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(mxh, mxl, myh, myl, d, ep);
   return (int)cudaGetLastError();
 }

@@ -116,6 +116,7 @@ struct WarpOp {
   int8_t gemm, X, Y, n_aux, n_out, gmask;   // gmask bit j: output j is the final S (global)
   int8_t rmask;                             // rmask bit j: output j is the final R (global)
   int8_t aux[kMaxAux], out[kMaxOut];
+  int8_t csync;                             // cluster kernel: full cluster barrier before the pushes
   float alpha[kMaxOut];
   float beta[kMaxOut][kMaxAux];
   float gamma[kMaxOut];
@@ -156,9 +157,18 @@ struct EpiParamsF32 {
   double alpha[kMaxOut];          // binary64: the epilogue combines in double, rounds once
   double beta[kMaxOut][kMaxAux];
   double gamma[kMaxOut];
+  // split-K of the last partial wave (set by launch_gemm_tf32x3 when sk_ws is given): pair tiles
+  // >= sk_first are computed as sk_split K ranges; the last CTA of a tile to finish adds the
+  // others' partial accumulators (sk_part) in K order and runs the epilogue
+  int sk_first, sk_split;
+  float* sk_part;
+  unsigned* sk_cnt;               // per CTA tile: [arrivals, partials written]
 };
+// bytes of split-K workspace launch_gemm_tf32x3 may use at size d (0: never splits); the first
+// 256 bytes hold counters that must be zero before the first launch (the kernel re-zeroes them)
+size_t tf32_splitk_ws_bytes(int d);
 int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
-                       const EpiParamsF32& ep, void* stream);
+                       const EpiParamsF32& ep, void* stream, void* sk_ws = nullptr);
 int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT, float* loT, int ld_out,
                      int d, bool identity, void* stream);
 int launch_axpby_f32(int d, const EpiParamsF32& ep, void* stream);

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 
 #include "internal.h"
@@ -278,7 +279,8 @@ struct __align__(16) ClusterOp {
   double alpha[kMaxOut], beta[kMaxOut][kMaxAux], gamma[kMaxOut];
   int x, y, kind, n_aux, n_out, gmask, rmask, pad;   // kind: 0 axpby, 1 gemm, 2 X = I, 3 Y = I
   int aux[kMaxAux], out[kMaxOut];                      // offsets (doubles); out < 0: not kept
-  int push, pad2[3];                                   // bit q: output q is replicated (pushed)
+  int push, csync, wait_bar, tx;   // push bit q: output q replicated; wait_bar: op whose pushes to await
+                                   // first (-1: none); tx: bytes this CTA receives from this op's pushes
 };
 
 template <int NC>   // CTAs per cluster; each owns RPC = 64 / NC rows of every value
@@ -323,6 +325,8 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     c.pad = 0;
     for (int x = 0; x < kMaxAux; ++x) c.aux[x] = own_of(x < w.n_aux ? w.aux[x] : 0);
     c.push = 0;
+    c.csync = w.csync;
+    c.wait_bar = -1;
     for (int q = 0; q < kMaxOut; ++q) {
       const bool keep = q < w.n_out && w.out[q] != kWSlotNone;
       c.out[q] = keep ? own_of(w.out[q]) : -1;
@@ -331,7 +335,20 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
       c.gamma[q] = w.dgamma[q];
       for (int x = 0; x < kMaxAux; ++x) c.beta[q][x] = w.dbeta[q][x];
     }
+    c.tx = (NC - 1) * kLSlotD * 8 * __popc(c.push);
     sops[i] = c;
+  }
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sops + n_ops);   // one mbarrier per op
+  if (tid == 0) {
+    int last = -1;
+    for (int i = 0; i < n_ops; ++i) {
+      sops[i].wait_bar = last;          // pushes of the previous pushing op must have landed
+      if (sops[i].push) last = i;
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bars + i));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(b) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(sops[i].tx) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // A: every CTA holds all 64 rows (A is read as a right operand), zero padded
   for (int i = tid; i < kRSlotD; i += 256) {
@@ -347,6 +364,14 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #pragma unroll
     for (int c = 0; c < NC; ++c) asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer[c]) : "r"(base), "r"(c));
   }
+  const uint32_t bar_off = static_cast<uint32_t>(reinterpret_cast<char*>(bars) - reinterpret_cast<char*>(smc));
+  auto wait_bar = [&](int b) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bars + b));
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done) : "r"(a) : "memory");
+  };
   cluster.sync();
 #ifdef NSERIES_SMALL_PROFILE
   long long tp0 = clock64();
@@ -354,6 +379,11 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #endif
   for (int o = 0; o < n_ops; ++o) {
     const ClusterOp& op = sops[o];
+    // the replicated rows this op reads were pushed by earlier ops: wait for the latest pushing
+    // op's bytes (earlier ones were awaited at their turn); the CTA barrier orders this op's
+    // local writes after every warp's reads of the previous ops
+    if (op.wait_bar >= 0 && (o == 0 || sops[o - 1].wait_bar != op.wait_bar)) wait_bar(op.wait_bar);
+    __syncthreads();
     // KS independent partial accumulators per row block (k-steps s with s % KS == p)
     constexpr int KS = 4;
     double part[MB][KS][2];
@@ -388,9 +418,13 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     if (tid == 0 && rank == 0) g_small_prof[1 + 3 * o] = clock64() + (long long)(acc[0][0] * 0.0);
 #endif
     // epilogue on local rows; outputs read later as right operands are pushed to every peer's
-    // replica (same offset) -- no barrier needed before it: outputs never alias this op's
-    // operands (slots are not reused in place)
+    // replica (same offset) with st.async, completing on the peer's mbarrier of this op.  Outputs
+    // never alias this op's operands (slots are not reused in place); a replicated slot reused
+    // after a peer read it is safe once that peer's later pushes arrived (build_cluster_program
+    // marks csync where no such push lies in between)
+    if (op.csync) cluster.sync();
     const int n_aux = op.n_aux, n_out = op.n_out;
+    const uint32_t my_bar = bar_off + 8u * (uint32_t)o;
 #pragma unroll
     for (int i = 0; i < MB; ++i) {
       const int rl = i * 8 + g, row = r0 + rl;
@@ -418,8 +452,8 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #pragma unroll
             for (int c = 0; c < NC; ++c)
               if (c != rank)
-                asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(peer[c] + lo), "d"(v0), "d"(v1)
-                             : "memory");
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n"
+                             ::"r"(peer[c] + lo), "d"(v0), "d"(v1), "r"(peer[c] + my_bar) : "memory");
           }
         }
         double* gdst = (op.gmask & (1 << q)) ? S : ((op.rmask & (1 << q)) ? R : nullptr);
@@ -432,18 +466,21 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
 #ifdef NSERIES_SMALL_PROFILE
     if (tid == 0 && rank == 0) g_small_prof[2 + 3 * o] = clock64();
 #endif
-    cluster.sync();   // every pushed row is visible cluster-wide before the next op reads it
 #ifdef NSERIES_SMALL_PROFILE
     if (tid == 0 && rank == 0) g_small_prof[3 + 3 * o] = clock64();
 #endif
   }
+  // no CTA leaves while pushes into it are in flight
+  for (int o = 0; o < n_ops; ++o)
+    if (sops[o].push) wait_bar(o);
+  cluster.sync();
 }
 
 template <int NC>
 int launch_cluster_nc(int d, const WarpProgram& prog, const double* A, double* S, double* R, cudaStream_t stream) {
   constexpr int kLSlotD = (64 / NC) * 64;
   const size_t smem = ((size_t)prog.n_slots * kLSlotD + (size_t)(prog.n_rep + 1) * 4096) * sizeof(double) +
-                      (size_t)prog.n_ops * sizeof(ClusterOp);
+                      (size_t)prog.n_ops * (sizeof(ClusterOp) + sizeof(uint64_t));
   if (smem > 227 * 1024) return -1;
   cudaError_t e = cudaFuncSetAttribute(plan_cluster_f64_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
@@ -468,11 +505,15 @@ nseries_status build_cluster_program(const Program& P, WarpProgram* out) {
     return P.val_kind[v] == V_TEMP || ((v == P.final_S || v == P.final_R) && last_use[v] >= 0);
   };
   // two pools, slots freed after the outputs of the op reading them last are placed
-  std::vector<int> slot(nv, -1);
-  std::vector<int> free_l, free_r;
-  int n_l = 0, n_r = 0;
+  std::vector<int> slot(nv, -1), last_y_read(nv, -1);
+  for (int i = 0; i < (int)P.ops.size(); ++i)
+    if (P.ops[i].gemm) last_y_read[P.ops[i].Y] = i;
+  std::vector<int> free_l, free_r, slot_read(128, -1);   // slot_read: last op reading the slot as Y
+  std::vector<char> csync(P.ops.size(), 0);
+  int n_l = 0, n_r = 0, last_push = -1;
   for (int i = 0; i < (int)P.ops.size(); ++i) {
     const Op& op = P.ops[i];
+    bool pushes = false;
     for (int j = 0; j < op.n_out; ++j) {
       const int v = op.out[j];
       if (!needs_slot(v)) continue;
@@ -481,7 +522,14 @@ nseries_status build_cluster_program(const Program& P, WarpProgram* out) {
       if (!fl.empty()) { sidx = fl.back(); fl.pop_back(); }
       else sidx = rep[v] ? n_r++ : n_l++;
       slot[v] = sidx;
+      if (rep[v]) {
+        // a peer may still read the previous occupant unless it pushed since (see the kernel)
+        if (slot_read[sidx] >= 0 && last_push < slot_read[sidx]) csync[i] = 1;
+        slot_read[sidx] = std::max(slot_read[sidx], last_y_read[v]);
+        pushes = true;
+      }
     }
+    if (pushes) last_push = i;
     for (int v = 0; v < nv; ++v)
       if (slot[v] >= 0 && ((last_use[v] == i && producer[v] < i) || (producer[v] == i && last_use[v] < 0)))
         (rep[v] ? free_r : free_l).push_back(slot[v]);
@@ -508,6 +556,7 @@ nseries_status build_cluster_program(const Program& P, WarpProgram* out) {
     w.n_aux = (int8_t)op.n_aux;
     w.n_out = (int8_t)op.n_out;
     w.gmask = 0;
+    w.csync = csync[i];
     w.rmask = 0;
     for (int a = 0; a < kMaxAux; ++a) w.aux[a] = a < op.n_aux ? (int8_t)code(op.aux[a]) : 0;
     for (int j = 0; j < kMaxOut; ++j) {

@@ -188,6 +188,19 @@ def test_config2_probes(h, steps):
     assert _probe_parity(S, A, steps, V, False) <= TOL64
 
 
+@pytest.mark.parametrize("d", [1024, 1100, 2100, 1024])
+def test_splitk_f32_deterministic(h, d):
+    # (the sizes alternate so the split-K counters left by one size are reused by another)
+    # split-K tiles sum their K-range partials in K order whichever CTA finishes last, so two
+    # evaluations are bit-identical; and they match the oracle on probe columns
+    A = inputs.random_matrix(d, 77, 0.9).astype(np.float32)
+    S1, _, _ = _run(h, A.astype(np.float64), [9, 9], dtype=torch.float32)
+    S2, _, _ = _run(h, A.astype(np.float64), [9, 9], dtype=torch.float32)
+    assert np.array_equal(S1, S2)
+    V, _ = inputs.probe_block(d, 5, n_unit=2, n_gauss=2)
+    assert _probe_parity(S1.astype(np.float64), A.astype(np.float64), [9, 9], V, False) <= TOL32
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("steps,sym", [([15, 15, 15], 0), ([9, 9, 9, 9], 0), ([2] * 12, 0), ([15, 15, 15], 1)])
 def test_config3_probes(h, steps, sym):
@@ -249,10 +262,12 @@ def test_parity_f32_flags_and_R(h, steps, extra):
         assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-5
 
 
-@pytest.mark.parametrize("d", [5, 128, 300, 1024, 2048, 4100])
+@pytest.mark.parametrize("d", [5, 128, 300, 1024, 1100, 2048, 4096, 4100])
 def test_matmul_engine_f32(h, d):
     # 4100: odd number of 128-row tiles (the second CTA of the last M-pair cluster lies past d)
-    # and a ragged last column tile
+    # and a ragged last column tile.  Split-K of the last partial wave (74 resident clusters):
+    # 1024 -> 16 pair tiles in 2 K ranges, 1100 -> 25 tiles in 2 uneven K ranges (69 k-blocks),
+    # 4096 -> the last 34 of 256 tiles in 2 K ranges
     # one 3xTF32 product vs the exact product of the fp32 inputs (<= 5e-7 budget)
     rng = np.random.default_rng(d + 7)
     X = rng.standard_normal((d, d)).astype(np.float32)
@@ -264,6 +279,19 @@ def test_matmul_engine_f32(h, d):
     cols = np.arange(d) if d <= 300 else rng.choice(d, 16, replace=False)
     ref = O.matvec(X.astype(np.float64), Y[:, cols].astype(np.float64))
     assert O.rel_fro(C.cpu().numpy()[:, cols], ref) <= 5e-7
+
+
+@pytest.mark.parametrize("d", [1024, 1100, 2100, 1024])
+def test_splitk_f32_deterministic(h, d):
+    # (the sizes alternate so the split-K counters left by one size are reused by another)
+    # split-K tiles sum their K-range partials in K order whichever CTA finishes last, so two
+    # evaluations are bit-identical; and they match the oracle on probe columns
+    A = inputs.random_matrix(d, 77, 0.9).astype(np.float32)
+    S1, _, _ = _run(h, A.astype(np.float64), [9, 9], dtype=torch.float32)
+    S2, _, _ = _run(h, A.astype(np.float64), [9, 9], dtype=torch.float32)
+    assert np.array_equal(S1, S2)
+    V, _ = inputs.probe_block(d, 5, n_unit=2, n_gauss=2)
+    assert _probe_parity(S1.astype(np.float64), A.astype(np.float64), [9, 9], V, False) <= TOL32
 
 
 @pytest.mark.slow
