@@ -402,7 +402,23 @@ def other_configs(P, h, stream):
     out["cfg5_d8192_fp64_k10000"] = {"plan": list(plan.step[:plan.n_steps]),
                                       "products": plan.products, "ms_per_eval": ms, "tflops": tf,
                                       "frac_of_fp64_peak": tf / FP64_PEAK_TFLOPS}
-    del A, S
+    # NEXT-3 row-sharded chain, config 5 in 8 row blocks, all on this GPU (device-copy gathers):
+    # the per-rank kernels of an 8-GPU run (1024 x 8192 x 8192 GEMMs) executed back to back
+    n = 8
+    blocks = [P.nseries_shard_rows(8192, n, s) for s in range(n)]
+    As = [A[r0:r0 + m].contiguous() for r0, m in blocks]
+    del S
+    Ss = [torch.empty_like(a) for a in As]
+    ms8 = _time_evals(lambda: P.nseries_eval_sharded(h, As, 0, n, 8192, 10000, plan=plan, S_shards=Ss, flags=fl,
+                                                     stream=stream), 1, 1, stream)
+    st = P.nseries_last_stats(h)
+    out["next3_sharded_cfg5_8blocks_1gpu"] = {
+        "blocks": n, "rows_per_block": blocks[0][1], "ms_per_eval": ms8, "gathers": st["gathers"],
+        "gathered_bytes_per_eval": st["gathers"] * 8192 * 8192 * 8,
+        "overhead_vs_dense": ms8 / ms - 1.0,
+        "note": "all row blocks on one GPU; an 8-rank run executes 1/8 of these launches per GPU plus "
+                "NCCL allgather-v gathers (not measurable on this 1-GPU box)"}
+    del A, As, Ss
     return out
 
 

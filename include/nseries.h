@@ -116,6 +116,7 @@ typedef struct {
   int32_t graph_replayed;  /* 1 if the last eval replayed a cached CUDA graph                */
   int32_t n_ops;
   float   ms_total;        /* device time of the last eval (NSERIES_SYNC_STATS only, else 0) */
+  int32_t gathers;         /* row-block gathers of the last nseries_eval_sharded (else 0)   */
 } nseries_stats;
 
 /* ---- lifecycle ---------------------------------------------------------------------- */
@@ -199,6 +200,42 @@ nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t
  * for accuracy micro-tests and peak measurement.  Counts as one product. */
 nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X, const void* Y,
                               void* C, int32_t d, void* stream);
+
+/* ---- row-sharded chain -----------------------------------
+ * One A too large (or too slow) for one GPU: rows [0, d) are split into `nshards` contiguous
+ * row blocks (nseries_shard_rows), and every value of the plan (A, the temporaries, S, R) is
+ * held as those row blocks.  A product X.Y needs, for its row block of the result, the row
+ * block of X and ALL of Y ("1D row-block shards with an allgather of the right
+ * operand per GEMM"); every value is a polynomial in A, so X.Y = Y.X and the executor gathers
+ * whichever factor is cheaper (I is never gathered: the identity buffer is full; A is gathered
+ * once; two gathered values are cached).  fp64 only (the DMMA engine with row-block launches).
+ *
+ * nseries_shard_rows: host-only, pure.  Shard s of nshards over d rows starts at
+ *   row0 = s*floor(d/nshards) + min(s, d mod nshards) and has floor(d/nshards) (+1 for the
+ *   first d mod nshards shards) rows.  INVALID_ARG unless 1 <= nshards <= d, 0 <= s < nshards.
+ * nseries_comm_unique_id / nseries_comm_init: the NCCL communicator the gathers run over
+ *   (libnccl.so.2 is opened at run time; the caller ships the 128-byte id from rank 0 to the
+ *   others over any side channel).  One rank per GPU; the handle keeps the
+ *   communicator until nseries_destroy.  CUDA error -> NSERIES_ERR_CUDA.
+ * nseries_eval_sharded: this process holds n_local consecutive shards first_shard ..
+ *   first_shard + n_local - 1 (HOST arrays of DEVICE pointers, each shard rows_s x d,
+ *   row-major, contiguous).  If the handle has a communicator with nshards == nranks *
+ *   n_local and first_shard == rank * n_local, each gather is an allgather-v (grouped
+ *   ncclBroadcast of every shard from its owner into the full-size buffer; with one rank all
+ *   broadcasts are local).  Otherwise every shard must be local (n_local == nshards) and the
+ *   gathers are device copies (one GPU; also the single-process test of the sharded
+ *   arithmetic); n_local < nshards without a matching communicator is INVALID_ARG.  S_shards / R_shards (nullable) receive the
+ *   row blocks of S and R.  Workspace per process: n_local x slots x (rows_max x d) doubles
+ *   plus three d x d buffers (gathered A and two gathered operands).  Same plans, flags and
+ *   product counts as nseries_eval (NSERIES_SYMMETRIC is rejected); eager launches (no
+ *   graph).  stats.launches counts GEMM/axpby launches, stats.gathers the gathers. */
+nseries_status nseries_shard_rows(int32_t d, int32_t nshards, int32_t shard, int32_t* row0, int32_t* rows);
+nseries_status nseries_comm_unique_id(void* id_out /* 128 bytes */);
+nseries_status nseries_comm_init(nseries_handle h, const void* id /* 128 bytes */, int32_t nranks, int32_t rank);
+nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shards, int32_t n_local,
+                                    int32_t first_shard, int32_t nshards, int32_t d, int64_t k,
+                                    const nseries_plan* plan, nseries_dtype dt, void* const* S_shards,
+                                    void* const* R_shards, uint32_t flags, void* stream);
 
 /* Statistics of the last eval on this handle (valid after the stream is synchronized). */
 nseries_status nseries_last_stats(nseries_handle h, nseries_stats* out);

@@ -30,7 +30,8 @@ EXPORTED = [
     "nseries_create", "nseries_destroy", "nseries_status_string", "nseries_version",
     "nseries_plan_build", "nseries_plan_finalize", "nseries_kernel_info", "nseries_eval",
     "nseries_eval_host", "nseries_eval_batched_strided", "nseries_eval_batched",
-    "nseries_matmul", "nseries_last_stats", "nseries_solve",
+    "nseries_matmul", "nseries_last_stats", "nseries_solve", "nseries_shard_rows",
+    "nseries_comm_unique_id", "nseries_comm_init", "nseries_eval_sharded",
 ]
 
 
@@ -54,7 +55,7 @@ class nseries_plan(ctypes.Structure):
 class nseries_stats(ctypes.Structure):
     _fields_ = [("products", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("graph_replayed", ctypes.c_int32), ("n_ops", ctypes.c_int32),
-                ("ms_total", ctypes.c_float)]
+                ("ms_total", ctypes.c_float), ("gathers", ctypes.c_int32)]
 
 
 class nseries_solve_info(ctypes.Structure):
@@ -101,6 +102,11 @@ def load_library(path=None):
         "nseries_last_stats": ([vp, ctypes.POINTER(nseries_stats)], ctypes.c_int),
         "nseries_solve": ([vp, vp, i32, i32, ctypes.c_double, i32, ctypes.c_int, vp, vp, u32, vp,
                            ctypes.POINTER(nseries_solve_info)], ctypes.c_int),
+        "nseries_shard_rows": ([i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)], ctypes.c_int),
+        "nseries_comm_unique_id": ([vp], ctypes.c_int),
+        "nseries_comm_init": ([vp, vp, i32, i32], ctypes.c_int),
+        "nseries_eval_sharded": ([vp, ctypes.POINTER(vp), i32, i32, i32, i32, i64, plan_p, ctypes.c_int,
+                                  ctypes.POINTER(vp), ctypes.POINTER(vp), u32, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -249,11 +255,48 @@ def nseries_solve(h, A, d, m, tol, max_steps=NSERIES_MAX_STEPS, Y=None, R_out=No
             "history": [info.history[i] for i in range(info.steps)]}
 
 
+def nseries_shard_rows(d, nshards, shard):
+    """(row0, rows) of row block `shard` of `nshards` over d rows (host-only)."""
+    r0, n = ctypes.c_int32(), ctypes.c_int32()
+    _check(load_library().nseries_shard_rows(int(d), int(nshards), int(shard), ctypes.byref(r0), ctypes.byref(n)),
+           "nseries_shard_rows")
+    return r0.value, n.value
+
+
+def nseries_comm_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it, the caller ships it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().nseries_comm_unique_id(buf), "nseries_comm_unique_id")
+    return buf.raw
+
+
+def nseries_comm_init(h, uid, nranks, rank):
+    if len(uid) != 128:
+        raise ValueError("NCCL unique id must be 128 bytes")
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(load_library().nseries_comm_init(h, buf, int(nranks), int(rank)), "nseries_comm_init")
+
+
+def nseries_eval_sharded(h, A_shards, first_shard, nshards, d, k, plan=None, S_shards=None, R_shards=None,
+                         flags=0, stream=None, dtype=NSERIES_F64):
+    """Row-sharded evaluation: A_shards / S_shards (/ R_shards) are lists of this process's row
+    blocks (device tensors), shards first_shard .. first_shard + len - 1 of nshards."""
+    n = len(A_shards)
+    arr = ctypes.c_void_p * n
+    a = arr(*[_ptr(x) for x in A_shards])
+    s_ = arr(*[_ptr(x) for x in S_shards])
+    r = arr(*[_ptr(x) for x in R_shards]) if R_shards is not None else None
+    st = load_library().nseries_eval_sharded(h, a, n, int(first_shard), int(nshards), int(d), int(k),
+                                             ctypes.byref(plan) if plan is not None else None, int(dtype), s_, r,
+                                             int(flags), _stream(stream))
+    _check(st, "nseries_eval_sharded")
+
+
 def nseries_last_stats(h):
     s = nseries_stats()
     _check(load_library().nseries_last_stats(h, ctypes.byref(s)), "nseries_last_stats")
     return {"products": s.products, "launches": s.launches, "graph_replayed": s.graph_replayed,
-            "n_ops": s.n_ops, "ms_total": s.ms_total}
+            "n_ops": s.n_ops, "ms_total": s.ms_total, "gathers": s.gathers}
 
 
 __all__ = [n for n in dir() if n.startswith(("nseries_", "NSERIES_"))] + [

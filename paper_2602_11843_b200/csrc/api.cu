@@ -1,7 +1,10 @@
 // api.cu -- C ABI (include/nseries.h): handle, workspace, plan compilation cache and the
 // stream executor that launches one fused GEMM kernel per op.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -46,6 +49,12 @@ struct nseries_ctx {
   // fp32 engine split-K workspace (tail-wave partial accumulators + per-tile counters)
   void* sk_ws = nullptr;
   size_t sk_bytes = 0;
+  // row-sharded chain (nseries_eval_sharded): NCCL communicator and the three d x d gather
+  // buffers (gathered A, two gathered right operands)
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  void* full = nullptr;
+  size_t full_bytes = 0;
 };
 
 namespace {
@@ -369,6 +378,180 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
 
 }  // namespace
 
+namespace {
+
+// ---------------------------------------------------------------- NCCL (opened at run time)
+// The library does not link NCCL: libnccl.so.2 is dlopen'ed on first use (the copy torch has
+// loaded if there is one, else the system library), so single-GPU use needs no NCCL at all.
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (lib) {
+      api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(lib, "ncclGetUniqueId"));
+      api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(lib, "ncclCommInitRank"));
+      api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(lib, "ncclCommDestroy"));
+      api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(lib, "ncclBroadcast"));
+      api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(lib, "ncclGroupStart"));
+      api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(lib, "ncclGroupEnd"));
+      api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(lib, "ncclGetErrorString"));
+      api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.broadcast && api.group_start &&
+               api.group_end && api.error_string;
+    }
+  }
+  return api;
+}
+
+nseries_status nccl_fail(nseries_ctx* h, ncclResult_t r) {
+  if (r == ncclSuccess) return NSERIES_OK;
+  std::fprintf(stderr, "[nseries] NCCL error: %s\n", nccl().error_string ? nccl().error_string(r) : "?");
+  if (h) h->sticky = NSERIES_ERR_CUDA;
+  return NSERIES_ERR_CUDA;
+}
+
+void shard_range(int d, int n, int s, int* row0, int* rows) {
+  const int q = d / n, r = d % n;
+  *row0 = s * q + (s < r ? s : r);
+  *rows = q + (s < r ? 1 : 0);
+}
+
+// Row-sharded executor (NEXT-3).  Values live as row blocks; before each product the right
+// factor is gathered into a full d x d buffer (allgather-v over NCCL, or device copies when
+// every shard is local), then every local row block runs the fused-epilogue DMMA GEMM on
+// (rows x d) x (d x d) with its identity terms offset by the block's first row.
+nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const* A_sh, double* const* S_sh,
+                           double* const* R_sh, int n_local, int first, int nshards, int d, cudaStream_t s,
+                           int* launches, int* gathers) {
+  // over NCCL whenever the handle's communicator matches the shard map (with one rank the
+  // broadcasts are all local: the single-GPU test of the collective path); else device copies
+  const bool remote = h->comm && nshards == h->nranks * n_local && first == h->rank * n_local;
+  int rows_max = 0;
+  std::vector<int> row0(nshards), rows(nshards);
+  for (int i = 0; i < nshards; ++i) {
+    shard_range(d, nshards, i, &row0[i], &rows[i]);
+    rows_max = std::max(rows_max, rows[i]);
+  }
+  const size_t slot = (size_t)rows_max * d;                 // doubles per row-block slot
+  const size_t dd = (size_t)d * d;
+  double* ws = static_cast<double*>(h->ws);
+  double* const A_full = static_cast<double*>(h->full);
+  double* const G[2] = {A_full + dd, A_full + 2 * dd};
+  double* const ident = static_cast<double*>(h->ident);
+  // row block j (local index) of value v
+  auto blk = [&](int v, int j) -> double* {
+    const int g = first + j;
+    switch (P.val_kind[v]) {
+      case V_USER_A: return const_cast<double*>(A_sh[j]);
+      case V_IDENT: return ident + (size_t)row0[g] * d;
+      case V_USER_S: return S_sh[j];
+      case V_USER_R: return R_sh ? R_sh[j] : nullptr;
+      default: return ws + ((size_t)j * P.n_slots + P.val_buf[v]) * slot;
+    }
+  };
+  int ng = 0, nl = 0;
+  auto gather = [&](int v, double* dst) -> nseries_status {
+    ++ng;
+    if (!remote) {
+      for (int j = 0; j < n_local; ++j) {
+        const int g = first + j;
+        cudaError_t e = cudaMemcpyAsync(dst + (size_t)row0[g] * d, blk(v, j), (size_t)rows[g] * d * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(h, e);
+      }
+      return NSERIES_OK;
+    }
+    // allgather-v: every shard broadcast from its owner into its rows of the full buffer
+    const NcclApi& nc = nccl();
+    ncclResult_t r = nc.group_start();
+    for (int g = 0; g < nshards && r == ncclSuccess; ++g) {
+      const int owner = g / n_local;
+      double* rows_dst = dst + (size_t)row0[g] * d;
+      const void* src = owner == h->rank ? blk(v, g - first) : rows_dst;
+      r = nc.broadcast(src, rows_dst, (size_t)rows[g] * d, ncclFloat64, owner, h->comm, s);
+    }
+    const ncclResult_t r2 = nc.group_end();
+    return nccl_fail(h, r != ncclSuccess ? r : r2);
+  };
+  // full copies: A once, two cached gathered values (values are immutable: cache by id)
+  bool a_full = false;
+  int cached[2] = {-1, -1}, lru = 0;
+  auto cost = [&](int v) {
+    const int kd = P.val_kind[v];
+    if (kd == V_IDENT) return 0;
+    if (kd == V_USER_A) return a_full ? 0 : 1;
+    return (cached[0] == v || cached[1] == v) ? 0 : 1;
+  };
+  auto full_of = [&](int v, const double** out) -> nseries_status {
+    const int kd = P.val_kind[v];
+    if (kd == V_IDENT) { *out = ident; return NSERIES_OK; }
+    if (kd == V_USER_A) {
+      if (!a_full) {
+        nseries_status st = gather(v, A_full);
+        if (st != NSERIES_OK) return st;
+        a_full = true;
+      }
+      *out = A_full;
+      return NSERIES_OK;
+    }
+    for (int b = 0; b < 2; ++b)
+      if (cached[b] == v) { lru = 1 - b; *out = G[b]; return NSERIES_OK; }
+    const int b = lru;
+    nseries_status st = gather(v, G[b]);
+    if (st != NSERIES_OK) return st;
+    cached[b] = v;
+    lru = 1 - b;
+    *out = G[b];
+    return NSERIES_OK;
+  };
+  for (size_t i = 0; i < P.ops.size(); ++i) {
+    const Op& op = P.ops[i];
+    int left = op.X, right = op.Y;
+    const double* Yf = nullptr;
+    if (op.gemm) {
+      // X.Y = Y.X: gather the cheaper factor (I and cached values cost nothing)
+      if (cost(op.X) < cost(op.Y)) std::swap(left, right);
+      nseries_status st = full_of(right, &Yf);
+      if (st != NSERIES_OK) return st;
+    }
+    for (int j = 0; j < n_local; ++j) {
+      const int g = first + j;
+      EpiParams ep{};
+      ep.rows = rows[g];
+      ep.row0 = row0[g];
+      ep.n_aux = op.n_aux;
+      ep.n_out = op.n_out;
+      for (int a = 0; a < op.n_aux; ++a) ep.aux[a] = blk(op.aux[a], j);
+      for (int o = 0; o < op.n_out; ++o) {
+        ep.out[o] = blk(op.out[o], j);
+        ep.alpha[o] = op.alpha[o];
+        ep.gamma[o] = op.gamma[o];
+        for (int a = 0; a < kMaxAux; ++a) ep.beta[o][a] = op.beta[o][a];
+      }
+      const int rc = op.gemm ? launch_gemm_f64(blk(left, j), Yf, d, ep, s) : launch_axpby_f64(d, ep, s);
+      if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+      ++nl;
+    }
+  }
+  *launches = nl;
+  *gathers = ng;
+  return NSERIES_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* nseries_status_string(nseries_status s) {
@@ -417,6 +600,8 @@ nseries_status nseries_destroy(nseries_handle h) {
   cudaDeviceSynchronize();
   if (h->ws) cudaFree(h->ws);
   if (h->sk_ws) cudaFree(h->sk_ws);
+  if (h->full) cudaFree(h->full);
+  if (h->comm && nccl().ok) nccl().comm_destroy(h->comm);
   if (h->ident) cudaFree(h->ident);
   if (h->stage) cudaFree(h->stage);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -540,6 +725,7 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     st = run(s);
     if (st != NSERIES_OK) return st;
   }
+  h->stats = nseries_stats{};
   h->stats.products = P.products;
   h->stats.launches = launches;
   h->stats.graph_replayed = replayed ? 1 : 0;
@@ -842,6 +1028,119 @@ nseries_status nseries_last_stats(nseries_handle h, nseries_stats* out) {
   if (!h || !out) return NSERIES_ERR_INVALID_ARG;
   *out = h->stats;
   return NSERIES_OK;
+}
+
+nseries_status nseries_shard_rows(int32_t d, int32_t nshards, int32_t shard, int32_t* row0, int32_t* rows) {
+  if (!row0 || !rows || nshards < 1 || d < nshards || shard < 0 || shard >= nshards) return NSERIES_ERR_INVALID_ARG;
+  int r0, n;
+  shard_range(d, nshards, shard, &r0, &n);
+  *row0 = r0;
+  *rows = n;
+  return NSERIES_OK;
+}
+
+nseries_status nseries_comm_unique_id(void* id_out) {
+  if (!id_out) return NSERIES_ERR_INVALID_ARG;
+  const NcclApi& nc = nccl();
+  if (!nc.ok) return NSERIES_ERR_CUDA;
+  ncclUniqueId id;
+  if (nc.get_unique_id(&id) != ncclSuccess) return NSERIES_ERR_CUDA;
+  std::memcpy(id_out, &id, sizeof(id));
+  return NSERIES_OK;
+}
+
+nseries_status nseries_comm_init(nseries_handle h, const void* id, int32_t nranks, int32_t rank) {
+  if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks) return NSERIES_ERR_INVALID_ARG;
+  if (h->sticky != NSERIES_OK) return h->sticky;
+  const NcclApi& nc = nccl();
+  if (!nc.ok) return NSERIES_ERR_CUDA;
+  cudaSetDevice(h->device);
+  if (h->comm) {
+    nc.comm_destroy(h->comm);
+    h->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  nseries_status st = nccl_fail(h, nc.comm_init_rank(&c, nranks, uid, rank));
+  if (st != NSERIES_OK) return st;
+  h->comm = c;
+  h->nranks = nranks;
+  h->rank = rank;
+  return NSERIES_OK;
+}
+
+nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shards, int32_t n_local,
+                                    int32_t first_shard, int32_t nshards, int32_t d, int64_t k,
+                                    const nseries_plan* plan, nseries_dtype dt, void* const* S_shards,
+                                    void* const* R_shards, uint32_t flags, void* stream) {
+  if (!h) return NSERIES_ERR_INVALID_ARG;
+  if (h->sticky != NSERIES_OK) return h->sticky;
+  if (!A_shards || !S_shards || n_local < 1 || nshards < n_local || d < nshards || k < 1 || first_shard < 0 ||
+      first_shard + n_local > nshards)
+    return NSERIES_ERR_INVALID_ARG;
+  if (dt != NSERIES_F64) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  if (flags & NSERIES_SYMMETRIC) return NSERIES_ERR_INVALID_ARG;
+  if (n_local < nshards && (!h->comm || nshards != h->nranks * n_local || first_shard != h->rank * n_local))
+    return NSERIES_ERR_INVALID_ARG;
+  for (int j = 0; j < n_local; ++j) {
+    if (!A_shards[j] || !S_shards[j]) return NSERIES_ERR_INVALID_ARG;
+    if (A_shards[j] == S_shards[j] || (R_shards && (!R_shards[j] || R_shards[j] == A_shards[j] ||
+                                                    R_shards[j] == S_shards[j])))
+      return NSERIES_ERR_ALIAS;
+  }
+  nseries_plan p;
+  nseries_status st = resolve_plan(plan, k, flags, &p);
+  if (st != NSERIES_OK) return st;
+  const bool want_R = R_shards != nullptr;
+  std::string key = plan_key(p, want_R);
+  auto it = h->programs.find(key);
+  if (it == h->programs.end()) {
+    Program prog;
+    st = compile_plan(p, want_R, &prog);
+    if (st != NSERIES_OK) return st;
+    it = h->programs.emplace(key, std::move(prog)).first;
+  }
+  const Program& P = it->second;
+  cudaSetDevice(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t rows_max = (size_t)(d + nshards - 1) / nshards;
+  st = ensure_ws(h, (size_t)n_local * P.n_slots * rows_max * d * sizeof(double));
+  if (st != NSERIES_OK) return st;
+  const size_t full_bytes = 3 * (size_t)d * d * sizeof(double);
+  if (full_bytes > h->full_bytes) {
+    if (h->full) {
+      cudaDeviceSynchronize();
+      cudaFree(h->full);
+      h->full = nullptr;
+      h->full_bytes = 0;
+    }
+    if (cudaMalloc(&h->full, full_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return NSERIES_ERR_OOM;
+    }
+    h->full_bytes = full_bytes;
+  }
+  st = ensure_identity(h, d, NSERIES_F64, s);    // I as a full right factor / its row blocks
+  if (st != NSERIES_OK) return st;
+  const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
+  if (timing) cudaEventRecord(h->ev0, s);
+  int launches = 0, gathers = 0;
+  st = run_sharded(h, P, reinterpret_cast<const double* const*>(A_shards), reinterpret_cast<double* const*>(S_shards),
+                   reinterpret_cast<double* const*>(R_shards), n_local, first_shard, nshards, d, s, &launches,
+                   &gathers);
+  if (st != NSERIES_OK) return st;
+  h->stats = nseries_stats{};
+  h->stats.products = P.products;
+  h->stats.launches = launches;
+  h->stats.n_ops = (int)P.ops.size();
+  h->stats.gathers = gathers;
+  if (timing) {
+    cudaEventRecord(h->ev1, s);
+    cudaEventSynchronize(h->ev1);
+    cudaEventElapsedTime(&h->stats.ms_total, h->ev0, h->ev1);
+  }
+  return cuda_fail(h, cudaGetLastError());
 }
 
 }  // extern "C"

@@ -73,7 +73,8 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 
   // ---- grouped raster: GROUP tile-rows per band
   constexpr int GROUP = 8;
-  const int ntm = (d + BM - 1) / BM, ntn = (d + BN - 1) / BN;
+  const int M = ep.rows > 0 ? ep.rows : d;   // rows of X / aux / outputs (row-sharded chain)
+  const int ntm = (M + BM - 1) / BM, ntn = (d + BN - 1) / BN;
   const int pid = blockIdx.x;
   int tm, tn;
   if constexpr (SYM) {
@@ -111,7 +112,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
       for (int q = tid; q < kChunksA; q += C::kThreads) {
         int r = q / (BK / 2), c = (q % (BK / 2)) * 2;
         int gr = m0 + r, gc = k0 + c;
-        bool ok = gr < d && gc < d;
+        bool ok = gr < M && gc < d;
         cp_async16(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok);
       }
       constexpr int kChunksB = BK * BN / 2;
@@ -127,7 +128,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
       for (int q = tid; q < BM * BK; q += C::kThreads) {
         int r = q / BK, c = q % BK;
         int gr = m0 + r, gc = k0 + c;
-        bool ok = gr < d && gc < d;
+        bool ok = gr < M && gc < d;
         cp_async8(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok);
       }
 #pragma unroll 4
@@ -203,7 +204,8 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #pragma unroll
   for (int i = 0; i < C::kMI; ++i) {
     const int row = m0 + wm0 + i * 8 + g;
-    if (row >= d) continue;
+    if (row >= M) continue;
+    const int grow = row + ep.row0;   // global row (identity terms)
 #pragma unroll
     for (int j = 0; j < C::kNI; ++j) {
       const int col = n0 + wn0 + j * 8 + 2 * t;
@@ -222,8 +224,8 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #pragma unroll
           for (int x = 0; x < kMaxAux; ++x)
             if (x < n_aux) { v0 += ep.beta[o][x] * av[x].x; v1 += ep.beta[o][x] * av[x].y; }
-          if (row == col) v0 += ep.gamma[o];
-          if (row == col + 1) v1 += ep.gamma[o];
+          if (grow == col) v0 += ep.gamma[o];
+          if (grow == col + 1) v1 += ep.gamma[o];
           double* const od = static_cast<double*>(ep.out[o]);
           if (!diag_tile) {
             if (o == ep.sumsq_out) ssq += (mirror ? 2.0 : 1.0) * (v0 * v0 + v1 * v1);
@@ -260,7 +262,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #pragma unroll
             for (int x = 0; x < kMaxAux; ++x)
               if (x < n_aux) v += ep.beta[o][x] * av[x];
-            if (row == col + e) v += ep.gamma[o];
+            if (grow == col + e) v += ep.gamma[o];
             if (diag_tile && row > col + e) continue;   // written by its mirror element
             const bool twice = mirror || (diag_tile && row < col + e);
             if (o == ep.sumsq_out) ssq += (twice ? 2.0 : 1.0) * v * v;
@@ -280,10 +282,10 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 
 // Degenerate epilogue without a product (k = 1 identity, elided k = 2 binary, R copy).
 __global__ void axpby_f64_kernel(int d, EpiParams ep) {
-  const size_t n = (size_t)d * d;
+  const size_t n = (size_t)(ep.rows > 0 ? ep.rows : d) * d;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < n;
        idx += (size_t)gridDim.x * blockDim.x) {
-    const int row = (int)(idx / d), col = (int)(idx % d);
+    const int row = (int)(idx / d) + ep.row0, col = (int)(idx % d);
     for (int o = 0; o < ep.n_out; ++o) {
       double v = 0.0;
       for (int x = 0; x < ep.n_aux; ++x) v += ep.beta[o][x] * static_cast<const double*>(ep.aux[x])[idx];
@@ -314,7 +316,8 @@ int launch_cfg_t(const double* X, const double* Y, int d, const EpiParams& ep, c
   }
   const int nt = (d + BM - 1) / BM;
   static_assert(BM == BN, "symmetric mode assumes square tiles");
-  const int tiles = SYM ? nt * (nt + 1) / 2 : nt * ((d + BN - 1) / BN);
+  const int M = ep.rows > 0 ? ep.rows : d;
+  const int tiles = SYM ? nt * (nt + 1) / 2 : ((M + BM - 1) / BM) * ((d + BN - 1) / BN);
   kern<<<tiles, C::kThreads, C::kSmem, s>>>(X, Y, d, ep);
   return (int)cudaGetLastError();
 }
@@ -335,8 +338,11 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   for (int i = 0; i < ep.n_out; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.out[i]) % 16 == 0;
   // Tile choice by wave efficiency: 128x128 (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs,
   // weighted by each config's measured per-SM efficiency (0.93 vs 0.82 of DMMA peak).
+  if (ep.sym && ep.rows > 0 && ep.rows != d) return (int)cudaErrorInvalidValue;
+  const int M = ep.rows > 0 ? ep.rows : d;
   const double nb = std::ceil(d / 128.0), ns = std::ceil(d / 64.0);
-  const double tb = ep.sym ? nb * (nb + 1) / 2 : nb * nb, ts = ep.sym ? ns * (ns + 1) / 2 : ns * ns;
+  const double mb = std::ceil(M / 128.0), ms = std::ceil(M / 64.0);
+  const double tb = ep.sym ? nb * (nb + 1) / 2 : mb * nb, ts = ep.sym ? ns * (ns + 1) / 2 : ms * ns;
   const double eb = 0.93 * tb / (std::ceil(tb / 148.0) * 148.0);
   const double es = 0.82 * ts / (std::ceil(ts / 296.0) * 296.0);
   if (eb >= es) {

@@ -85,6 +85,8 @@ struct EpiParams {
   int sym = 0;                   // symmetric mode: X, Y, aux and outputs are symmetric (polynomials
                                  // of a symmetric A); only tiles on/above the diagonal are computed
                                  // and each off-diagonal output tile is also stored transposed
+  int rows = 0;                  // row-sharded chain: X, aux and outputs are `rows` x d row blocks
+  int row0 = 0;                  // (0: rows = d) starting at global row row0 (I's diagonal offset)
 };
 
 // Batched small-matrix path: the compiled op list with values mapped to shared-memory slots.

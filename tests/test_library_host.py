@@ -120,3 +120,32 @@ def test_library_radix15_params_vs_oracle_polish(lib):
     assert len(nums) == 28
     for a, b in zip(nums, ref):
         assert abs(a - b) <= 2e-16 * max(1.0, abs(b))
+
+
+# ---------------------------------------------------------------- row shards (NEXT-3), host-only
+
+@pytest.mark.parametrize("d,n", [(1, 1), (7, 7), (100, 3), (1100, 8), (4096, 8), (8192, 3), (16384, 8)])
+def test_shard_rows_partition(lib, d, n):
+    # contiguous, disjoint, covering [0, d), sizes differ by at most one, larger blocks first
+    blocks = [P.nseries_shard_rows(d, n, s) for s in range(n)]
+    assert blocks[0][0] == 0
+    for (r0, m), (r1, _) in zip(blocks, blocks[1:]):
+        assert r0 + m == r1
+    assert blocks[-1][0] + blocks[-1][1] == d
+    sizes = [m for _, m in blocks]
+    assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True) and min(sizes) >= 1
+
+
+@pytest.mark.parametrize("d,n,s", [(5, 0, 0), (5, 6, 0), (5, 2, 2), (5, 2, -1), (0, 1, 0)])
+def test_shard_rows_rejects(lib, d, n, s):
+    with pytest.raises(P.NSeriesError) as e:
+        P.nseries_shard_rows(d, n, s)
+    assert e.value.status == 1
+
+
+def test_eval_sharded_rejects_without_device(lib):
+    # argument checks happen before any device work: a NULL handle is INVALID_ARG
+    import ctypes
+    arr = (ctypes.c_void_p * 1)(None)
+    st = lib.nseries_eval_sharded(None, arr, 1, 0, 1, 8, 4, None, 0, arr, None, 0, None)
+    assert st == 1
