@@ -37,10 +37,20 @@
 namespace nseries {
 namespace {
 
+#ifndef NSERIES_TF32_XACC
+#define NSERIES_TF32_XACC 0   // cross terms hi*lo + lo*hi in their own TMEM accumulator (below);
+#endif                        // needs BN = 128: d = 4096 GEMM 0.717 -> 0.802 ms, d = 1024 0.054 -> 0.040
 #ifndef NSERIES_TF32_BN
+#if NSERIES_TF32_XACC
+#define NSERIES_TF32_BN 128
+#define NSERIES_TF32_BK 32
+#define NSERIES_TF32_STAGES 3
+#define NSERIES_TF32_KSC 4
+#else
 #define NSERIES_TF32_BN 256   // (BN = 192 -- 4.76 waves instead of 3.46 at d = 4096 -- measured
 #define NSERIES_TF32_BK 16    //  11% slower: lower operand reuse per TMA byte)
 #define NSERIES_TF32_STAGES 4
+#endif
 #endif
 #ifndef NSERIES_TF32_CLUSTER
 #define NSERIES_TF32_CLUSTER 2   // CTA pairs along M share (TMA-multicast) the B operand tile
@@ -70,7 +80,13 @@ constexpr int kPrefetchKB = NSERIES_TF32_PREFETCH;   // L2 prefetch distance (k-
 #endif
 constexpr int KSC = NSERIES_TF32_KSC;        // k-steps (of 8) per accumulation chunk (Kc = 8 KSC)
 constexpr int CPS = (BK / 8) / KSC;          // chunks per smem stage
-constexpr int NBUF = 512 / BN;               // TMEM chunk accumulators of BN columns
+// XACC: the cross terms (hi*lo + lo*hi, ~2^-11 of the product) accumulate over the whole K
+// range in one TMEM accumulator -- their truncation bias is ~2^-11 of a full-K chain, far below
+// fp32 rounding -- and only the hi*hi chunks (KSC MMAs each) go through the per-chunk drain.
+// Same bias per chunk as KSC = 2 with all three terms, with half the drains per K.
+constexpr bool XACC = NSERIES_TF32_XACC != 0;
+constexpr int NBUF = XACC ? (512 - BN) / BN : 512 / BN;   // TMEM chunk accumulators of BN columns
+static_assert(!XACC || !TWO_SM, "cross accumulator: 1-SM MMAs only");
 #ifndef NSERIES_TF32_EPI_WARPS
 #define NSERIES_TF32_EPI_WARPS 8   // (16: 11% slower -- the single MMA-issue thread competes with 20 warps)
 #endif
@@ -82,7 +98,7 @@ constexpr int kFinalWarps = kThreads / 32;    // every warp runs the final epilo
 constexpr uint32_t kATileBytes = BM * BK * 4;   // 8 KB  (128 rows x 16 k)
 constexpr uint32_t kBTileBytes = BN * BK * 4;   // 8 KB (128 rows of Y^T x 16 k)
 constexpr uint32_t kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
-constexpr uint32_t kTmemCols = NBUF * BN <= 256 ? 256 : 512;   // allocation: power of two >= used
+constexpr uint32_t kTmemCols = (NBUF + (XACC ? 1 : 0)) * BN <= 256 ? 256 : 512;   // power of two >= used
 constexpr uint32_t kSwizzleLayout = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / _64B
 constexpr uint32_t kAtomBytes = 8 * BK * 4;     // 8 rows x 64 B = 512 B (SBO)
 constexpr int kStageLd = EC + 1;                // epilogue staging row (floats)
@@ -657,6 +673,25 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
           }
           mma2_commit_mc_w(&sm.tmem_full[b], 3);   // both CTAs' accumulators ready
           if (h == CPS - 1) mma2_commit_mc_w(&sm.empty[s], 3);
+        } else if constexpr (XACC) {
+          // hi*hi into this chunk's buffer, then the cross terms into the full-K accumulator
+          const uint32_t t_x = tmem + NBUF * BN;
+#pragma unroll
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma_tf32_w(t_acc, dxh + 2 * ks, dyh + 2 * ks, j == 0 ? 0u : 1u);
+          }
+#pragma unroll
+          for (int j = 0; j < KSC; ++j) {
+            const int ks = h * KSC + j;
+            mma_tf32_w(t_x, dxh + 2 * ks, dyl + 2 * ks, (c == 0 && j == 0) ? 0u : 1u);
+            mma_tf32_w(t_x, dxl + 2 * ks, dyh + 2 * ks, 1u);
+          }
+          mma_commit_w(&sm.tmem_full[b]);          // chunk accumulator ready for the epilogue
+          if (h == CPS - 1) {
+            if (CL > 1) mma_commit_mc_w(&sm.empty[s], (1u << CL) - 1);
+            else mma_commit_w(&sm.empty[s]);
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < KSC; ++j) {
@@ -745,6 +780,22 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       if (lane == 0) {
         if constexpr (TWO_SM) mbar_arrive_cluster(mapa_rank(saddr(&sm.tmem_empty[b]), 0));   // leader's
         else mbar_arrive(&sm.tmem_empty[b]);
+      }
+    }
+    if constexpr (XACC) {
+      // the last chunk's commit covered every MMA: the cross accumulator is complete
+      const uint32_t t_x = tmem + lane_off + NBUF * BN + cb;
+#pragma unroll
+      for (int j = 0; j < EC / 32; ++j) {
+        uint32_t v[16], w[16];
+        tmem_ld16_async(t_x + 32 * j, v);
+        tmem_ld16_async(t_x + 32 * j + 16, w);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          fadd2(acc[32 * j + i], acc[32 * j + i + 1], __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          fadd2(acc[32 * j + 16 + i], acc[32 * j + 16 + i + 1], __uint_as_float(w[i]), __uint_as_float(w[i + 1]));
+        }
       }
     }
 #ifdef NSERIES_TF32_DEBUG
