@@ -5,7 +5,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libnseries.so")
+_LIB_PATH = os.environ.get("NSERIES_LIB") or os.path.join(_PKG, "libnseries.so")   # NSERIES_LIB: harness A/B builds
 
 NSERIES_OK = 0
 STATUS_NAMES = {
