@@ -10,7 +10,7 @@ int main(int argc, char** argv) {
   const int batch = 16384, d = 32;
   nseries_plan plan{};
   plan.n_steps = 2; plan.step[0] = 9; plan.step[1] = 9;
-  if (nseries_plan_finalize(&plan, 81, 0) != NSERIES_OK) { printf("plan fail\n"); return 1; }
+  if (finalize_plan(&plan, 81, 0) != NSERIES_OK) { printf("plan fail\n"); return 1; }
   Program P;
   if (compile_plan(plan, false, &P) != NSERIES_OK) { printf("compile fail\n"); return 1; }
   WarpProgram wp;
