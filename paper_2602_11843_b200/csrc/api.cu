@@ -393,11 +393,9 @@ struct NcclApi {
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
 };
-const NcclApi& nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+NcclApi load_nccl() {
+  NcclApi api;
+  {
     void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (lib) {
@@ -412,6 +410,10 @@ const NcclApi& nccl() {
                api.group_end && api.error_string;
     }
   }
+  return api;
+}
+const NcclApi& nccl() {
+  static const NcclApi api = load_nccl();   // thread-safe one-time initialisation
   return api;
 }
 
