@@ -307,13 +307,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2, bool SYM>
 int launch_cfg_t(const double* X, const double* Y, int d, const EpiParams& ep, cudaStream_t s) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
   auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2, SYM>;
-  static bool attr_set = false;   // per template instance
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::kSmem);
-    if (e != cudaSuccess) return (int)e;
-    attr_set = true;
-  }
+  if (int e = smem_attr_once<gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2, SYM>>((int)C::kSmem)) return e;
   const int nt = (d + BM - 1) / BM;
   static_assert(BM == BN, "symmetric mode assumes square tiles");
   const int M = ep.rows > 0 ? ep.rows : d;

@@ -997,7 +997,7 @@ int wave_clusters() {
     cfg.gridDim = dim3(148 * CL);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = sizeof(Smem) + 1024;
-    cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    smem_attr_once<gemm_tf32x3_kernel>((int)cfg.dynamicSmemBytes);
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, gemm_tf32x3_kernel, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
@@ -1076,12 +1076,7 @@ int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const 
   if (!rc) rc = g_maps.get(Yl, d, ldp, 1, &myl);
   if (rc) return rc;
   const size_t smem = sizeof(Smem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    attr = true;
-  }
+  if (int e = smem_attr_once<gemm_tf32x3_kernel>((int)smem)) return e;
   const int row_groups = ((d + BM - 1) / BM + CL - 1) / CL;   // clusters of CL row tiles
   const int ntn = (d + BN - 1) / BN;
   if (ep.sym && CL * BM != BN) return (int)cudaErrorInvalidValue;   // square pair tiles needed

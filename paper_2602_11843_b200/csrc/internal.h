@@ -3,6 +3,10 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <atomic>
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#endif
 #include <vector>
 
 #include "../../include/nseries.h"
@@ -71,6 +75,23 @@ int assign_slots_inplace(const Program& P, const std::vector<bool>& needs_slot,
                          std::vector<int>* slot_of_value, bool inplace = true);
 // last op index reading value v (operand or aux), -1 if never read
 std::vector<int> value_last_use(const Program& P);
+
+#ifdef __CUDACC__
+// Opt a kernel into more than 48 KB of dynamic shared memory once per (kernel, device): the
+// attribute is per device, so a process driving several GPUs sets it on each.
+template <auto Kern>
+inline int smem_attr_once(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return (int)e;
+  done.fetch_or(bit, std::memory_order_release);
+  return 0;
+}
+#endif
 
 // ---------------------------------------------------------------- device engines
 struct EpiParams {

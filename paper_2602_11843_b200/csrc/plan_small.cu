@@ -110,12 +110,7 @@ plan_small_f64_kernel(int d, const __grid_constant__ SmallProgram prog) {
 int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream) {
   if (d > 64 || prog.n_ops > kMaxSmallOps) return -1;
   const size_t smem = 2 * 64 * kLd * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(plan_small_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    attr = true;
-  }
+  if (int e = smem_attr_once<plan_small_f64_kernel>((int)smem)) return e;
   plan_small_f64_kernel<<<1, kSmallThreads, smem, static_cast<cudaStream_t>(stream)>>>(d, prog);
   return (int)cudaGetLastError();
 }
