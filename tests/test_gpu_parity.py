@@ -421,3 +421,20 @@ def test_large_ragged_d(h, dt):
     S, _, _ = _run(h, A, steps, dtype=torch.float64 if dt == "f64" else torch.float32)
     err = _probe_parity(S.astype(np.float64), A, steps, V, False)
     assert err <= (TOL64 if dt == "f64" else 2e-5), err
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dt,d", [("f64", 16384), ("f32", 16384), ("f64", 20000)])
+def test_largest_sizes(h, dt, d):
+    # beyond the BASELINE configs: d = 16384 (2 GiB per fp64 matrix, 4096 tiles of 128^2, 64
+    # k-tiles per CTA ... 512 in the fp32 engine) and d = 20000 (ragged: 157 tiles per side);
+    # k = 9 by radix-9 (5 products), 4 seeded probe columns against the long-double oracle
+    steps = [9]
+    rng = np.random.default_rng(d)
+    A = (0.6 / np.sqrt(d)) * rng.standard_normal((d, d))
+    if dt == "f32":
+        A = A.astype(np.float32).astype(np.float64)
+    V, _ = inputs.probe_block(d, 7, n_unit=2, n_gauss=2)
+    S, _, _ = _run(h, A, steps, dtype=torch.float64 if dt == "f64" else torch.float32)
+    err = _probe_parity(S.astype(np.float64), A, steps, V, False)
+    assert err <= (TOL64 if dt == "f64" else 2e-5), err
