@@ -414,6 +414,7 @@ def other_configs(P, h, stream):
     st = P.nseries_last_stats(h)
     out["next3_sharded_cfg5_8blocks_1gpu"] = {
         "blocks": n, "rows_per_block": blocks[0][1], "ms_per_eval": ms8, "gathers": st["gathers"],
+        "gathers_prefetched": st["gathers_prefetched"],
         "gathered_bytes_per_eval": st["gathers"] * 8192 * 8192 * 8,
         "overhead_vs_dense": ms8 / ms - 1.0,
         "note": "all row blocks on one GPU; an 8-rank run executes 1/8 of these launches per GPU plus "

@@ -117,6 +117,7 @@ typedef struct {
   int32_t n_ops;
   float   ms_total;        /* device time of the last eval (NSERIES_SYNC_STATS only, else 0) */
   int32_t gathers;         /* row-block gathers of the last nseries_eval_sharded (else 0)   */
+  int32_t gathers_prefetched; /* of which issued ahead, overlapping the previous product    */
 } nseries_stats;
 
 /* ---- lifecycle ---------------------------------------------------------------------- */

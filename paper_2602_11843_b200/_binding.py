@@ -55,7 +55,8 @@ class nseries_plan(ctypes.Structure):
 class nseries_stats(ctypes.Structure):
     _fields_ = [("products", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("graph_replayed", ctypes.c_int32), ("n_ops", ctypes.c_int32),
-                ("ms_total", ctypes.c_float), ("gathers", ctypes.c_int32)]
+                ("ms_total", ctypes.c_float), ("gathers", ctypes.c_int32),
+                ("gathers_prefetched", ctypes.c_int32)]
 
 
 class nseries_solve_info(ctypes.Structure):
@@ -296,7 +297,8 @@ def nseries_last_stats(h):
     s = nseries_stats()
     _check(load_library().nseries_last_stats(h, ctypes.byref(s)), "nseries_last_stats")
     return {"products": s.products, "launches": s.launches, "graph_replayed": s.graph_replayed,
-            "n_ops": s.n_ops, "ms_total": s.ms_total, "gathers": s.gathers}
+            "n_ops": s.n_ops, "ms_total": s.ms_total, "gathers": s.gathers,
+            "gathers_prefetched": s.gathers_prefetched}
 
 
 __all__ = [n for n in dir() if n.startswith(("nseries_", "NSERIES_"))] + [

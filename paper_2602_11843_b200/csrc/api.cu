@@ -55,6 +55,8 @@ struct nseries_ctx {
   int nranks = 1, rank = 0;
   void* full = nullptr;
   size_t full_bytes = 0;
+  cudaStream_t gather_stream = nullptr;      // prefetching gathers run here
+  cudaEvent_t ev_gready = nullptr, ev_gdone[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -436,7 +438,7 @@ void shard_range(int d, int n, int s, int* row0, int* rows) {
 // (rows x d) x (d x d) with its identity terms offset by the block's first row.
 nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const* A_sh, double* const* S_sh,
                            double* const* R_sh, int n_local, int first, int nshards, int d, cudaStream_t s,
-                           int* launches, int* gathers) {
+                           int* launches, int* gathers, int* prefetched) {
   // over NCCL whenever the handle's communicator matches the shard map (with one rank the
   // broadcasts are all local: the single-GPU test of the collective path); else device copies
   const bool remote = h->comm && nshards == h->nranks * n_local && first == h->rank * n_local;
@@ -463,14 +465,14 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
       default: return ws + ((size_t)j * P.n_slots + P.val_buf[v]) * slot;
     }
   };
-  int ng = 0, nl = 0;
-  auto gather = [&](int v, double* dst) -> nseries_status {
+  int ng = 0, nl = 0, npf = 0;
+  auto gather = [&](int v, double* dst, cudaStream_t gs) -> nseries_status {
     ++ng;
     if (!remote) {
       for (int j = 0; j < n_local; ++j) {
         const int g = first + j;
         cudaError_t e = cudaMemcpyAsync(dst + (size_t)row0[g] * d, blk(v, j), (size_t)rows[g] * d * sizeof(double),
-                                        cudaMemcpyDeviceToDevice, s);
+                                        cudaMemcpyDeviceToDevice, gs);
         if (e != cudaSuccess) return cuda_fail(h, e);
       }
       return NSERIES_OK;
@@ -482,26 +484,50 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
       const int owner = g / n_local;
       double* rows_dst = dst + (size_t)row0[g] * d;
       const void* src = owner == h->rank ? blk(v, g - first) : rows_dst;
-      r = nc.broadcast(src, rows_dst, (size_t)rows[g] * d, ncclFloat64, owner, h->comm, s);
+      r = nc.broadcast(src, rows_dst, (size_t)rows[g] * d, ncclFloat64, owner, h->comm, gs);
     }
     const ncclResult_t r2 = nc.group_end();
     return nccl_fail(h, r != ncclSuccess ? r : r2);
   };
-  // full copies: A once, two cached gathered values (values are immutable: cache by id)
+  // producer op of every value (-1: A, I or never produced)
+  std::vector<int> producer(P.n_values, -1);
+  for (size_t i = 0; i < P.ops.size(); ++i)
+    for (int o = 0; o < P.ops[i].n_out; ++o) producer[P.ops[i].out[o]] = (int)i;
+  // full copies: A once, two gathered values (values are immutable: cached by id).  A gather
+  // for the NEXT product whose factor already exists runs on the gather stream while the
+  // current product computes (prefetch); pending[b] marks a buffer whose gather the main
+  // stream has not yet waited for.
   bool a_full = false;
-  int cached[2] = {-1, -1}, lru = 0;
+  int cached[2] = {-1, -1}, lru = 0;          // lru: the buffer to overwrite next
+  bool pending[2] = {false, false};
+  if (!h->ev_gready) {
+    cudaError_t e = cudaEventCreateWithFlags(&h->ev_gready, cudaEventDisableTiming);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) e = cudaEventCreateWithFlags(&h->ev_gdone[b], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+  }
   auto cost = [&](int v) {
     const int kd = P.val_kind[v];
     if (kd == V_IDENT) return 0;
     if (kd == V_USER_A) return a_full ? 0 : 1;
     return (cached[0] == v || cached[1] == v) ? 0 : 1;
   };
+  // X.Y = Y.X: gather the cheaper factor; on a tie the one produced earlier (prefetchable)
+  auto right_of = [&](const Op& op) -> int {
+    const int cx = cost(op.X), cy = cost(op.Y);
+    if (cx != cy) return cx < cy ? op.X : op.Y;
+    return producer[op.X] < producer[op.Y] ? op.X : op.Y;
+  };
+  auto wait_pending = [&](int b) -> nseries_status {
+    if (!pending[b]) return NSERIES_OK;
+    pending[b] = false;
+    return cuda_fail(h, cudaStreamWaitEvent(s, h->ev_gdone[b], 0));
+  };
   auto full_of = [&](int v, const double** out) -> nseries_status {
     const int kd = P.val_kind[v];
     if (kd == V_IDENT) { *out = ident; return NSERIES_OK; }
     if (kd == V_USER_A) {
       if (!a_full) {
-        nseries_status st = gather(v, A_full);
+        nseries_status st = gather(v, A_full, s);
         if (st != NSERIES_OK) return st;
         a_full = true;
       }
@@ -509,9 +535,15 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
       return NSERIES_OK;
     }
     for (int b = 0; b < 2; ++b)
-      if (cached[b] == v) { lru = 1 - b; *out = G[b]; return NSERIES_OK; }
-    const int b = lru;
-    nseries_status st = gather(v, G[b]);
+      if (cached[b] == v) {
+        lru = 1 - b;
+        nseries_status st = wait_pending(b);
+        *out = G[b];
+        return st;
+      }
+    const int b = lru;                          // stream order protects earlier readers
+    nseries_status st = wait_pending(b);
+    if (st == NSERIES_OK) st = gather(v, G[b], s);
     if (st != NSERIES_OK) return st;
     cached[b] = v;
     lru = 1 - b;
@@ -522,11 +554,38 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
     const Op& op = P.ops[i];
     int left = op.X, right = op.Y;
     const double* Yf = nullptr;
+    int cur_buf = -1;
     if (op.gemm) {
-      // X.Y = Y.X: gather the cheaper factor (I and cached values cost nothing)
-      if (cost(op.X) < cost(op.Y)) std::swap(left, right);
+      right = right_of(op);
+      left = right == op.X ? op.Y : op.X;
       nseries_status st = full_of(right, &Yf);
       if (st != NSERIES_OK) return st;
+      cur_buf = Yf == G[0] ? 0 : (Yf == G[1] ? 1 : -1);
+    }
+    // prefetch: the next product's gathered factor, if it exists before this op runs, into
+    // the buffer this op does not read (the previous op's reads are ordered by the event)
+    if (i + 1 < P.ops.size() && P.ops[i + 1].gemm) {
+      const Op& nx = P.ops[i + 1];
+      const int r2 = right_of(nx);
+      const int b2 = cur_buf == 0 ? 1 : 0;
+      if (cost(r2) && P.val_kind[r2] != V_USER_A && producer[r2] < (int)i) {
+        if (!h->gather_stream && cudaStreamCreateWithFlags(&h->gather_stream, cudaStreamNonBlocking) != cudaSuccess)
+          return cuda_fail(h, cudaGetLastError());
+        nseries_status st = wait_pending(b2);   // (no-op: only one gather is ever in flight)
+        if (st != NSERIES_OK) return st;
+        // everything issued so far on the main stream (incl. reads of buffer b2) precedes it
+        cudaError_t e = cudaEventRecord(h->ev_gready, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->gather_stream, h->ev_gready, 0);
+        if (e != cudaSuccess) return cuda_fail(h, e);
+        st = gather(r2, G[b2], h->gather_stream);
+        if (st != NSERIES_OK) return st;
+        ++npf;
+        e = cudaEventRecord(h->ev_gdone[b2], h->gather_stream);
+        if (e != cudaSuccess) return cuda_fail(h, e);
+        cached[b2] = r2;
+        pending[b2] = true;
+        lru = 1 - b2;
+      }
     }
     for (int j = 0; j < n_local; ++j) {
       const int g = first + j;
@@ -547,8 +606,13 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
       ++nl;
     }
   }
+  for (int b = 0; b < 2; ++b) {                 // the caller's stream owns everything at exit
+    nseries_status st = wait_pending(b);
+    if (st != NSERIES_OK) return st;
+  }
   *launches = nl;
   *gathers = ng;
+  *prefetched = npf;
   return NSERIES_OK;
 }
 
@@ -610,6 +674,10 @@ nseries_status nseries_destroy(nseries_handle h) {
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev_S) cudaEventDestroy(h->ev_S);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->gather_stream) cudaStreamDestroy(h->gather_stream);
+  if (h->ev_gready) cudaEventDestroy(h->ev_gready);
+  for (cudaEvent_t e : h->ev_gdone)
+    if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
@@ -1127,16 +1195,17 @@ nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shard
   if (st != NSERIES_OK) return st;
   const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
   if (timing) cudaEventRecord(h->ev0, s);
-  int launches = 0, gathers = 0;
+  int launches = 0, gathers = 0, prefetched = 0;
   st = run_sharded(h, P, reinterpret_cast<const double* const*>(A_shards), reinterpret_cast<double* const*>(S_shards),
                    reinterpret_cast<double* const*>(R_shards), n_local, first_shard, nshards, d, s, &launches,
-                   &gathers);
+                   &gathers, &prefetched);
   if (st != NSERIES_OK) return st;
   h->stats = nseries_stats{};
   h->stats.products = P.products;
   h->stats.launches = launches;
   h->stats.n_ops = (int)P.ops.size();
   h->stats.gathers = gathers;
+  h->stats.gathers_prefetched = prefetched;
   if (timing) {
     cudaEventRecord(h->ev1, s);
     cudaEventSynchronize(h->ev1);

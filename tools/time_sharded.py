@@ -45,4 +45,5 @@ for n in (1, 2, 8):
     st = P.nseries_last_stats(h)
     out[f"sharded{n}_ms"] = round(ms, 3)
     out[f"sharded{n}_gathers"] = st["gathers"]
+    out[f"sharded{n}_prefetched"] = st["gathers_prefetched"]
 print(json.dumps(out))
