@@ -124,6 +124,8 @@ def test_sharded_config3():
         Sd, _ = _dense(hh, A, [15, 15, 15])
         assert O.rel_fro(S, Sd) <= 1e-12
         assert st["products"] == 18
+        # gathers of factors that exist before the preceding product are issued ahead of it
+        assert st["gathers"] == 14 and st["gathers_prefetched"] == 2
     finally:
         P.nseries_destroy(hh)
 
