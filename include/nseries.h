@@ -89,6 +89,11 @@ typedef enum {
                                          product computes only the tiles on/above the diagonal and
                                          mirrors them (same products, ~half the tile work).  The
                                          result is unspecified if A is not symmetric.           */
+#define NSERIES_HOST_ASYNC       0x40u/* nseries_eval_host only: return without synchronizing;
+                                         consecutive calls alternate two device staging sets so
+                                         the copy-in of one matrix overlaps the evaluation of the
+                                         previous one.  S_host / R_host are valid and A_host may
+                                         be reused only after nseries_host_sync.                */
 
 #define NSERIES_MAX_STEPS 128
 
@@ -156,10 +161,14 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
                             uint32_t flags, void* stream);
 
 /* Same with HOST pointers: copies A host->device, evaluates, copies S (and R_out) back,
- * then synchronizes `stream`.  Pinned host memory gives asynchronous copies. */
+ * then synchronizes `stream`.  Pinned host memory gives asynchronous copies.  With
+ * NSERIES_HOST_ASYNC the call only enqueues (copy-in on a private stream, the evaluation on
+ * `stream`, copy-out on a private stream, ordered by events) and a stream of calls pipelines
+ * copy-in / evaluate / copy-out across matrices; nseries_host_sync waits for all of them. */
 nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d, int64_t k,
                                  const nseries_plan* plan, nseries_dtype dt, void* S_host,
                                  void* R_host, uint32_t flags, void* stream);
+nseries_status nseries_host_sync(nseries_handle h);
 
 /* Batched small-matrix path: `batch` independent d x d matrices (d <= 64), A_b at
  * A + b*strideA elements, S_b at S + b*strideS.  One kernel launch evaluates the whole plan

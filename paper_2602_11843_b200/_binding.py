@@ -23,6 +23,7 @@ NSERIES_RFORM_TELESCOPE = 0x4
 NSERIES_NO_GRAPH = 0x8
 NSERIES_SYNC_STATS = 0x10
 NSERIES_SYMMETRIC = 0x20
+NSERIES_HOST_ASYNC = 0x40
 NSERIES_MAX_STEPS = 128
 
 # every symbol include/nseries.h declares (tests check the .so exports exactly these)
@@ -31,7 +32,7 @@ EXPORTED = [
     "nseries_plan_build", "nseries_plan_finalize", "nseries_kernel_info", "nseries_eval",
     "nseries_eval_host", "nseries_eval_batched_strided", "nseries_eval_batched",
     "nseries_matmul", "nseries_last_stats", "nseries_solve", "nseries_shard_rows",
-    "nseries_comm_unique_id", "nseries_comm_init", "nseries_eval_sharded",
+    "nseries_comm_unique_id", "nseries_comm_init", "nseries_eval_sharded", "nseries_host_sync",
 ]
 
 
@@ -105,6 +106,7 @@ def load_library(path=None):
                            ctypes.POINTER(nseries_solve_info)], ctypes.c_int),
         "nseries_shard_rows": ([i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)], ctypes.c_int),
         "nseries_comm_unique_id": ([vp], ctypes.c_int),
+        "nseries_host_sync": ([vp], ctypes.c_int),
         "nseries_comm_init": ([vp, vp, i32, i32], ctypes.c_int),
         "nseries_eval_sharded": ([vp, ctypes.POINTER(vp), i32, i32, i32, i32, i64, plan_p, ctypes.c_int,
                                   ctypes.POINTER(vp), ctypes.POINTER(vp), u32, vp], ctypes.c_int),
@@ -217,6 +219,11 @@ def nseries_eval_host(h, A, d, k, plan=None, dtype=None, S=None, R_out=None, fla
                                           ctypes.byref(plan) if plan is not None else None,
                                           dt, _ptr(S), _ptr(R_out), int(flags), _stream(stream))
     _check(st, "nseries_eval_host")
+
+
+def nseries_host_sync(h):
+    """Wait for every NSERIES_HOST_ASYNC nseries_eval_host call on this handle."""
+    _check(load_library().nseries_host_sync(h), "nseries_host_sync")
 
 
 def nseries_eval_batched_strided(h, A, strideA, batch, d, k, plan=None, dtype=None, S=None,

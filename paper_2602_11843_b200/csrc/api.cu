@@ -55,6 +55,13 @@ struct nseries_ctx {
   int nranks = 1, rank = 0;
   void* full = nullptr;
   size_t full_bytes = 0;
+  // NSERIES_HOST_ASYNC: two device staging sets, a copy-in stream and per-set events
+  void* astage[2] = {nullptr, nullptr};
+  size_t astage_bytes = 0;
+  int aset = 0;
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_evaldone[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaStream_t last_eval_stream = nullptr;
   cudaStream_t gather_stream = nullptr;      // prefetching gathers run here
   cudaEvent_t ev_gready = nullptr, ev_gdone[2] = {nullptr, nullptr};
 };
@@ -675,6 +682,13 @@ nseries_status nseries_destroy(nseries_handle h) {
   if (h->ev_S) cudaEventDestroy(h->ev_S);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->gather_stream) cudaStreamDestroy(h->gather_stream);
+  if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
+  for (int b = 0; b < 2; ++b) {
+    if (h->astage[b]) cudaFree(h->astage[b]);
+    if (h->ev_in[b]) cudaEventDestroy(h->ev_in[b]);
+    if (h->ev_evaldone[b]) cudaEventDestroy(h->ev_evaldone[b]);
+    if (h->ev_out[b]) cudaEventDestroy(h->ev_out[b]);
+  }
   if (h->ev_gready) cudaEventDestroy(h->ev_gready);
   for (cudaEvent_t e : h->ev_gdone)
     if (e) cudaEventDestroy(e);
@@ -817,6 +831,62 @@ nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d
   const size_t bytes = (size_t)d * d * elem_size(dt);
   const size_t need = bytes * (R_host ? 3 : 2);
   cudaSetDevice(h->device);
+  if (flags & NSERIES_HOST_ASYNC) {
+    // pipelined: set b's copy-in waits for the previous evaluation that read set b; that
+    // evaluation's successor on set b waits for set b's copy-out
+    if (!h->h2d_stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking);
+      if (e == cudaSuccess && !h->copy_stream) e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+      for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_evaldone[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) return cuda_fail(h, e);
+      for (int b = 0; b < 2; ++b) {      // recorded once so the first waits are satisfied
+        cudaEventRecord(h->ev_evaldone[b], h->h2d_stream);
+        cudaEventRecord(h->ev_out[b], h->h2d_stream);
+      }
+    }
+    if (need > h->astage_bytes) {
+      nseries_host_sync(h);
+      for (int b = 0; b < 2; ++b) {
+        if (h->astage[b]) cudaFree(h->astage[b]);
+        h->astage[b] = nullptr;
+      }
+      h->astage_bytes = 0;
+      for (int b = 0; b < 2; ++b)
+        if (cudaMalloc(&h->astage[b], need) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
+      h->astage_bytes = need;
+    }
+    const int b = h->aset;
+    h->aset ^= 1;
+    char* dA = static_cast<char*>(h->astage[b]);
+    char* dS = dA + bytes;
+    char* dR = R_host ? dS + bytes : nullptr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    h->last_eval_stream = s;
+    cudaError_t e = cudaStreamWaitEvent(h->h2d_stream, h->ev_evaldone[b], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A_host, bytes, cudaMemcpyHostToDevice, h->h2d_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_in[b], h->h2d_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->ev_in[b], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->ev_out[b], 0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    h->want_ev_S = true;
+    nseries_status st = nseries_eval(h, dA, d, k, plan, dt, dS, dR, flags & ~(NSERIES_SYNC_STATS | NSERIES_HOST_ASYNC),
+                                     stream);
+    h->want_ev_S = false;
+    if (st != NSERIES_OK) return st;
+    e = cudaEventRecord(h->ev_evaldone[b], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->copy_stream, h->ev_S, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(S_host, dS, bytes, cudaMemcpyDeviceToHost, h->copy_stream);
+    if (e == cudaSuccess && R_host) {
+      e = cudaStreamWaitEvent(h->copy_stream, h->ev_evaldone[b], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(R_host, dR, bytes, cudaMemcpyDeviceToHost, h->copy_stream);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_out[b], h->copy_stream);
+    return cuda_fail(h, e);
+  }
   if (need > h->stage_bytes) {
     if (h->stage) { cudaDeviceSynchronize(); cudaFree(h->stage); h->stage = nullptr; h->stage_bytes = 0; }
     if (cudaMalloc(&h->stage, need) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
@@ -847,6 +917,16 @@ nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(h, e);
   return cuda_fail(h, cudaStreamSynchronize(h->copy_stream));
+}
+
+nseries_status nseries_host_sync(nseries_handle h) {
+  if (!h) return NSERIES_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  cudaError_t e = cudaSuccess;
+  for (cudaStream_t st : {h->h2d_stream, h->last_eval_stream, h->copy_stream})
+    if (st && e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (!h->last_eval_stream && e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+  return cuda_fail(h, e);
 }
 
 static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t strideA,

@@ -407,6 +407,33 @@ def test_host_api_overlapped_copy_out(h, d, steps, dt, flags):
         assert np.all(np.isfinite(Rh))
 
 
+@pytest.mark.parametrize("d,dt", [(200, "f64"), (300, "f32"), (40, "f64")])
+def test_host_api_async_pipeline(h, d, dt):
+    # NSERIES_HOST_ASYNC: 5 different matrices through nseries_eval_host without synchronizing
+    # (two staging sets alternate, copy-in of matrix i+1 overlaps evaluation i); after
+    # nseries_host_sync every S_i and R_i equals the synchronous call's bits and the oracle
+    steps = [9, 2]
+    k = OP.plan_reaches(steps)
+    plan = P.nseries_plan_finalize(steps, k, 0)
+    npdt = np.float32 if dt == "f32" else np.float64
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    As = [torch.from_numpy(inputs.random_matrix(d, 40 + i, 0.7).astype(npdt)).pin_memory() for i in range(5)]
+    Ss = [torch.full_like(a, float("nan")).pin_memory() for a in As]
+    Rs = [torch.full_like(a, float("nan")).pin_memory() for a in As]
+    for a, s_, r in zip(As, Ss, Rs):
+        P.nseries_eval_host(h, a, d, k, plan=plan, S=s_, R_out=r, flags=P.NSERIES_HOST_ASYNC, dtype=P.NSERIES_F32 if dt == "f32" else P.NSERIES_F64)
+    P.nseries_host_sync(h)
+    tol = 2e-5 if dt == "f32" else TOL64
+    for a, s_, r in zip(As, Ss, Rs):
+        Sy = torch.empty_like(a)
+        Ry = torch.empty_like(a)
+        P.nseries_eval_host(h, a, d, k, plan=plan, S=Sy, R_out=Ry)
+        assert torch.equal(s_, Sy) and torch.equal(r, Ry)
+        ref = _oracle_full(a.numpy().astype(np.float64), steps)
+        assert O.rel_fro(s_.numpy().astype(np.float64), ref) <= tol
+    assert tdt == As[0].dtype
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("dt", ["f64", "f32"])
 def test_large_ragged_d(h, dt):
