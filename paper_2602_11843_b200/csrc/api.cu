@@ -627,6 +627,12 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
 
 extern "C" {
 
+static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t strideA,
+                                        const void* const* A_ptrs, int32_t batch, int32_t d,
+                                        int64_t k, const nseries_plan* plan, nseries_dtype dt,
+                                        void* S, int64_t strideS, void* const* S_ptrs,
+                                        uint32_t flags, void* stream);
+
 const char* nseries_status_string(nseries_status s) {
   switch (s) {
     case NSERIES_OK: return "ok";
@@ -742,6 +748,19 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
       if (p.step[i] == 15) p.form[i] = 2;
   }
   const bool want_R = R_out != nullptr;
+  if (dt == NSERIES_F32 && d <= 64 && !want_R && !(flags & NSERIES_SYNC_STATS)) {
+    // a small fp32 matrix runs the whole plan in ONE launch of the batched kernels (batch 1:
+    // warp-group kernel for d <= 32, CTA kernel above) instead of ~2 launches per product of
+    // the tiled engine (d = 32: 107 -> 17 us); same radix-15 residual form as the tiled path
+    nseries_plan p1 = p;
+    p1.flags |= NSERIES_RFORM_TELESCOPE;
+    const nseries_status bst = eval_batched_impl(h, A, (int64_t)d * d, nullptr, 1, d, k, &p1, dt, S,
+                                                 (int64_t)d * d, nullptr, flags, stream);
+    if (bst != NSERIES_ERR_UNSUPPORTED_SIZE) {
+      if (bst == NSERIES_OK && h->want_ev_S) cudaEventRecord(h->ev_S, static_cast<cudaStream_t>(stream));
+      return bst;
+    }
+  }
   std::string key = plan_key(p, want_R);
   auto it = h->programs.find(key);
   if (it == h->programs.end()) {
