@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -43,8 +44,9 @@ struct nseries_ctx {
   cudaStream_t cap_stream = nullptr;
   struct CachedGraph { cudaGraphExec_t exec; int launches; };
   std::map<std::string, CachedGraph> graphs;
-  // small fp64 single-matrix kernels (d <= 64): 0 cluster (default) -> 1 single-CTA shared
-  // memory -> 2 single-CTA global slots; NSERIES_SMALL_MODE selects the first one tried
+  // small fp64 single-matrix kernels (d <= 64), tried in order: 2-D cluster, 1-D cluster,
+  // single-CTA shared memory, single-CTA global slots.  NSERIES_SMALL_MODE selects the first
+  // one tried: 0 (2-D cluster, default), 3 (1-D cluster), 1 (shared memory), 2 (global)
   int small_mode = 0;
   // fp32 engine split-K workspace (tail-wave partial accumulators + per-tile counters)
   void* sk_ws = nullptr;
@@ -320,7 +322,21 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
                            int d, nseries_dtype dt, cudaStream_t s, int* launches, bool sym = false) {
   if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
   if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode == 0) {
-    // 4-CTA cluster, each CTA a 16-row block of every value (DSMEM for the operand rows)
+    // 4 x 2 cluster, each CTA a 16 x 32 block of every product (row / column views, DSMEM pushes)
+    auto c2 = std::make_unique<C2Program>();   // ~8 KB: heap, copied into the launch parameters
+    if (build_cluster2d_program(P, c2.get()) == NSERIES_OK) {
+      const int rc = launch_plan_cluster2d_f64(d, *c2, static_cast<const double*>(A), static_cast<double*>(S),
+                                               static_cast<double*>(R), s);
+      if (rc == 0) {
+        if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
+        *launches = 1;
+        return NSERIES_OK;
+      }
+      if (rc != -1) return cuda_fail(h, (cudaError_t)rc);
+    }
+  }
+  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && (h->small_mode == 0 || h->small_mode == 3)) {
+    // 8-CTA cluster, each CTA an 8-row block of every value (right factors replicated)
     WarpProgram wp{};
     if (build_cluster_program(P, &wp) == NSERIES_OK) {
       const int rc = launch_plan_cluster_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
@@ -333,7 +349,7 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
       if (rc != -1) return cuda_fail(h, (cudaError_t)rc);
     }
   }
-  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode <= 1) {
+  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && (h->small_mode <= 1 || h->small_mode == 3)) {
     // whole plan with every value in shared memory (falls through if the live set is too big)
     WarpProgram wp{};
     if (build_warp_program(P, &wp) == NSERIES_OK) {

@@ -220,6 +220,29 @@ int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double
 // Cluster of 4 CTAs, each holding a 16-row block of every value (operand rows of the other CTAs
 // read through distributed shared memory); prog built with inplace = false.  -1 if unsupported.
 int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
+// 2-D cluster kernel (plan_cluster2d.cu): CTA (r, c) of an RB x CB cluster owns the 64/RB x
+// 64/CB block (r, c) of every product.  A value read as a LEFT factor lives in "row views"
+// (the CTA's 64/RB rows, all 64 columns, replicated across its row group), one read as a RIGHT
+// factor in "column views" (all rows, the CTA's 64/CB columns, replicated across its column
+// group), an aux-only value in an own-block slot.  Slot indices per pool, -1 = none.
+struct C2Op {
+  int8_t kind, n_aux, n_out, gmask, rmask, csync;   // kind: 0 axpby, 1 gemm, 2 X = I, 3 Y = I
+  int8_t aux_kind[kMaxAux];                         // 0 row view, 1 column view, 2 own block
+  int16_t x, y;                                     // row-view slot of X, column-view slot of Y
+  int16_t aux_slot[kMaxAux];
+  int16_t out_row[kMaxOut], out_col[kMaxOut], out_own[kMaxOut];
+  double alpha[kMaxOut];
+  double beta[kMaxOut][kMaxAux];
+  double gamma[kMaxOut];
+};
+struct C2Program {
+  int n_ops, n_row, n_col, n_own;
+  int a_row, a_col;                                 // slots A is loaded into (-1: not needed)
+  C2Op ops[kMaxBatchedOps];
+};
+nseries_status build_cluster2d_program(const Program& P, C2Program* out);
+int launch_plan_cluster2d_f64(int d, const C2Program& prog, const double* A, double* S, double* R, void* stream);
+
 // Slot layout for the cluster kernel: values read as a right operand live in slots replicated in
 // every CTA (each CTA pushes its rows of such outputs to all peers); the others in per-CTA
 // row-block slots.  No in-place reuse.

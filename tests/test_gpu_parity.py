@@ -317,21 +317,22 @@ def _handle_with_small_mode(mode):
 
 @pytest.fixture(scope="module")
 def h_small_modes():
-    """Handles forced onto each single-launch small kernel: 0 = 4-CTA cluster (default),
-    1 = single-CTA shared-memory values, 2 = single-CTA global slots."""
-    hs = {m: _handle_with_small_mode(m) for m in (0, 1, 2)}
+    """Handles forced onto each single-launch small kernel: 0 = 4 x 2 cluster (default),
+    3 = 8-CTA row-split cluster, 1 = single-CTA shared-memory values, 2 = single-CTA global
+    slots."""
+    hs = {m: _handle_with_small_mode(m) for m in (0, 1, 2, 3)}
     yield hs
     for x in hs.values():
         P.nseries_destroy(x)
 
 
-@pytest.mark.parametrize("d", [5, 33, 64])
+@pytest.mark.parametrize("d", [1, 5, 17, 33, 64])
 @pytest.mark.parametrize("steps,extra", [([9, 9], 0), ([9, 9], 1), ([15, 15], 0), ([15, 1, 5], 2),
                                          ([5, 5, 5], 1), ([1, 2, 2], 0), ([1], 0), ([2], 1), ([3, 1, 9], 2)])
-@pytest.mark.parametrize("which", [0, 1, 2])
+@pytest.mark.parametrize("which", [0, 3, 1, 2])
 def test_small_kernels_flags_and_R(h_small_modes, d, steps, extra, which):
-    # the three single-launch small kernels (cluster / shared-memory values / global slots), with
-    # the elide / telescoping flags and the residual output R_out
+    # the four single-launch small kernels (2-D cluster / row-split cluster / shared-memory
+    # values / global slots), with the elide / telescoping flags and the residual output R_out
     flags = [0, P.NSERIES_ELIDE_TRIVIAL, P.NSERIES_RFORM_TELESCOPE][extra]
     handle = h_small_modes[which]
     A = inputs.random_matrix(d, 11 + d, 0.7)
