@@ -33,6 +33,10 @@
 namespace nseries {
 namespace {
 
+#ifdef NSERIES_C2_PROFILE
+__device__ long long g_c2_prof[256];   // harness-only (tools/c2_probe.cu): per-op phase clocks
+#endif
+
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c[0]), "+d"(c[1])
@@ -46,8 +50,11 @@ __device__ __forceinline__ void cp8(double* smem, const double* g, bool ok) {
 
 // row view (RPC x 64): fragment loads read rows g, columns 4s + t -> XOR-swizzle in 4s
 __device__ __forceinline__ int swz_row(int r, int c) { return r * 64 + (c ^ (4 * ((r & 3) ^ ((r & 1) << 1)))); }
-// column view / own block (rows x 32): fragment loads read rows 4s + t, columns 8j + g
-__device__ __forceinline__ int swz_col(int r, int c) { return r * 32 + (c ^ (8 * (r & 3))); }
+// column view / own block (rows x 32): fragment loads read rows 4s + t, columns 8j + g.  A
+// double's bank pair is set by its column mod 16 (a 32-double row spans 64 banks), so the XOR
+// moves the four rows of a k-step to the four 4-column groups: each half-warp hits 16 distinct
+// bank pairs
+__device__ __forceinline__ int swz_col(int r, int c) { return r * 32 + (c ^ (4 * (r & 3))); }
 
 struct C2Dev {                      // an op with resolved shared-memory offsets (doubles)
   int kind, n_aux, n_out, gmask, rmask, csync, wait_bar, tx;
@@ -163,13 +170,20 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
   const int rl = 8 * mt + g;                 // this lane's block row (epilogue) / A-fragment row
   const int cl = 8 * nt + 2 * t;             // this lane's block column pair (epilogue)
   const int grow = r0 + rl;
+#ifdef NSERIES_C2_PROFILE
+  if (tid == 0 && rank == 0) g_c2_prof[0] = clock64();
+#endif
   for (int o = 0; o < n_ops; ++o) {
     const C2Dev& op = sops[o];
     if (op.wait_bar >= 0 && (o == 0 || sops[o - 1].wait_bar != op.wait_bar)) wait_bar(op.wait_bar);
     __syncthreads();
-    double part[4][2];
+#ifdef NSERIES_C2_PROFILE
+    if (tid == 0 && rank == 0) g_c2_prof[1 + 3 * o] = clock64();
+#endif
+    constexpr int KS = 8;                    // independent partial accumulators (DMMA latency)
+    double part[KS][2];
 #pragma unroll
-    for (int p = 0; p < 4; ++p) part[p][0] = part[p][1] = 0.0;
+    for (int p = 0; p < KS; ++p) part[p][0] = part[p][1] = 0.0;
     if (op.kind != 0) {
       const bool xi = op.kind == 2, yi = op.kind == 3;
       const double* X = smc + op.x;
@@ -180,12 +194,17 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
         const int k = 4 * s + t;
         const double a = xi ? ((grow == k && grow < d) ? 1.0 : 0.0) : X[swz_row(rl, k)];
         const double b = yi ? ((k == c0 + bcol && k < d) ? 1.0 : 0.0) : Y[swz_col(k, bcol)];
-        dmma884(part[s & 3], a, b);
+        dmma884(part[s % KS], a, b);
       }
     }
     double acc[2];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) acc[e] = (part[0][e] + part[1][e]) + (part[2][e] + part[3][e]);
+    for (int e = 0; e < 2; ++e)
+      acc[e] = ((part[0][e] + part[1][e]) + (part[2][e] + part[3][e])) +
+               ((part[4][e] + part[5][e]) + (part[6][e] + part[7][e]));
+#ifdef NSERIES_C2_PROFILE
+    if (tid == 0 && rank == 0) g_c2_prof[2 + 3 * o] = clock64() + (long long)(acc[0] * 0.0);
+#endif
     if (op.csync) cluster.sync();
     const uint32_t my_bar = bar_off + 8u * (uint32_t)o;
     double2 av[kMaxAux];
@@ -241,6 +260,9 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
         if (gcol + 1 < d) gdst[(size_t)grow * d + gcol + 1] = v1;
       }
     }
+#ifdef NSERIES_C2_PROFILE
+    if (tid == 0 && rank == 0) g_c2_prof[3 + 3 * o] = clock64();
+#endif
   }
   // no CTA leaves while pushes into it are in flight
   for (int o = 0; o < n_ops; ++o)
