@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "internal.h"
@@ -309,7 +310,7 @@ int launch_cfg_t(const double* X, const double* Y, int d, const EpiParams& ep, c
   auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2, SYM>;
   if (int e = smem_attr_once<gemm_f64_kernel<BM, BN, BK, WM, WN, STAGES, V2, SYM>>((int)C::kSmem)) return e;
   const int nt = (d + BM - 1) / BM;
-  static_assert(BM == BN, "symmetric mode assumes square tiles");
+  static_assert(!SYM || BM == BN, "symmetric mode assumes square tiles");
   const int M = ep.rows > 0 ? ep.rows : d;
   const int tiles = SYM ? nt * (nt + 1) / 2 : ((M + BM - 1) / BM) * ((d + BN - 1) / BN);
   kern<<<tiles, C::kThreads, C::kSmem, s>>>(X, Y, d, ep);
@@ -330,16 +331,24 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   bool v2 = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
   for (int i = 0; i < ep.n_aux; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.aux[i]) % 16 == 0;
   for (int i = 0; i < ep.n_out; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.out[i]) % 16 == 0;
-  // Tile choice by wave efficiency: 128x128 (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs,
-  // weighted by each config's measured per-SM efficiency (0.93 vs 0.82 of DMMA peak).
+  // Tile choice by modelled efficiency: 128x128 (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs
+  // (NSERIES_F64_TILE = 1 / 3 forces one, harness only).
   if (ep.sym && ep.rows > 0 && ep.rows != d) return (int)cudaErrorInvalidValue;
   const int M = ep.rows > 0 ? ep.rows : d;
   const double nb = std::ceil(d / 128.0), ns = std::ceil(d / 64.0);
   const double mb = std::ceil(M / 128.0), ms = std::ceil(M / 64.0);
   const double tb = ep.sym ? nb * (nb + 1) / 2 : mb * nb, ts = ep.sym ? ns * (ns + 1) / 2 : ms * ns;
-  const double eb = 0.93 * tb / (std::ceil(tb / 148.0) * 148.0);
-  const double es = 0.82 * ts / (std::ceil(ts / 296.0) * 296.0);
-  if (eb >= es) {
+  // Model fitted to tools/time_f64_tiles.py (fraction of the DMMA peak per tile config):
+  // 128x128 tiles run one CTA per SM at ~0.935 with whole-wave quantisation; 64x64 tiles run
+  // two CTAs per SM (~0.87 together, ~0.73 for a lone CTA) and, from two waves up, fill the
+  // tail well enough that ~0.87 holds (d = 2048: 0.87 measured vs 0.79 for 128x128).
+  const double eb = 0.935 * tb / (std::ceil(tb / 148.0) * 148.0);
+  double es;
+  if (ts >= 2 * 296) es = 0.87;
+  else if (ts > 148) es = (ts / 148.0) / (2.0 * std::ceil(ts / 296.0) / 0.87);
+  else es = 0.73 * ts / 148.0;
+  static const int force = std::getenv("NSERIES_F64_TILE") ? std::atoi(std::getenv("NSERIES_F64_TILE")) : 0;
+  if (force == 1 || (force == 0 && eb >= es)) {
     return v2 ? launch_cfg<128, 128, 32, 64, 32, 3, true>(X, Y, d, ep, s)
               : launch_cfg<128, 128, 32, 64, 32, 3, false>(X, Y, d, ep, s);
   }
