@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-plan", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs 1/2/4 side lines")
+    ap.add_argument("--sharded", action="store_true",
+                    help="NEXT-3: config 5 (d = 8192, k = 10000) row-sharded across the N ranks "
+                         "(strong scaling; not the headline line)")
     return ap.parse_args()
 
 
@@ -440,10 +443,65 @@ def _traffic():
     return None
 
 
+def run_sharded(args):
+    """One A (config 5) split into N row blocks, one per rank, gathers over NCCL (NEXT-3)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_setup(args.gpus)
+    import paper_2602_11843_b200 as P
+    from paper_2602_11843_b200 import inputs
+    torch.cuda.set_device(local)
+    h = P.nseries_create(local)
+    d, k = 8192, 10000
+    uid = [P.nseries_comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    P.nseries_comm_init(h, uid[0], world, rank)
+    A = inputs.cfg5(device="cuda")
+    r0, rows = P.nseries_shard_rows(d, world, rank)
+    A_blk = A[r0:r0 + rows].contiguous()
+    del A
+    S_blk = torch.empty_like(A_blk)
+    fl = P.NSERIES_ALLOW_APPROX
+    plan = P.nseries_plan_build(k, P.NSERIES_PLAN_AUTO, [15, 9, 5, 2], fl)
+    stream = torch.cuda.current_stream()
+    run = lambda: P.nseries_eval_sharded(h, [A_blk], rank, world, d, k, plan=plan, S_shards=[S_blk], flags=fl,
+                                         stream=stream)
+    for _ in range(max(args.warmup, 1)):
+        run()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(1, args.steps // 5)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(n):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / n
+    st = P.nseries_last_stats(h)
+    if rank == 0:
+        tf = plan.products * 2.0 * d ** 3 / (ms * 1e-3) / 1e12
+        print(json.dumps({
+            "metric": "S_k(A) evals/sec, one config-5 matrix row-sharded over the ranks (NEXT-3)",
+            "value": 1e3 / ms, "unit": "evals/s", "n_gpus": world, "steps": n, "warmup": max(args.warmup, 1),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "cfg5 d=8192 k=10000 AUTO plan, row-sharded",
+                                           "d": d, "k": k, "plan": list(plan.step[:plan.n_steps]),
+                                           "products": plan.products, "parallelism": f"row-shard{world}"},
+            "tflops": tf, "frac_of_fp64_peak_per_gpu": tf / world / FP64_PEAK_TFLOPS,
+            "gathers": st["gathers"], "gathers_prefetched": st["gathers_prefetched"]}))
+    P.nseries_destroy(h)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.sharded:
+        return run_sharded(args)
     return run_native(args)
 
 
