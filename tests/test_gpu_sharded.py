@@ -73,7 +73,7 @@ def _dense(h, A, steps, want_R=False, extra=0):
     return S.cpu().numpy(), (R.cpu().numpy() if want_R else None)
 
 
-@pytest.mark.parametrize("d", [65, 200, 1100])
+@pytest.mark.parametrize("d", [9, 40, 65, 200, 1100])
 @pytest.mark.parametrize("n", [1, 2, 3, 8])
 @pytest.mark.parametrize("steps", [[9, 9], [15, 15], [2] * 6, [15, 1, 5], [5, 1, 9], [3, 3]])
 def test_sharded_equals_dense(h, d, n, steps):
