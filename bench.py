@@ -411,6 +411,28 @@ def other_configs(P, h, stream):
     out["cfg5_d8192_fp64_k10000"] = {"plan": list(plan.step[:plan.n_steps]),
                                       "products": plan.products, "ms_per_eval": ms, "tflops": tf,
                                       "frac_of_fp64_peak": tf / FP64_PEAK_TFLOPS}
+    # the paper's own Table 3 workload (d = 500, normal A, fp64): ms per method
+    # on this GPU beside the paper's CPU times (context only) and the normal
+    # residual ||I - (I - A) S||_F of the returned S (the paper's accuracy column)
+    import numpy as np
+    A3, _, _ = inputs.table3_matrix()
+    A3t = torch.from_numpy(A3).cuda()
+    S3 = torch.empty_like(A3t)
+    rows3 = [("binary", [2] * 7, 128, 8), ("binary", [2] * 9, 512, 10), ("quinary", [5] * 3, 125, 8),
+             ("quinary", [5] * 4, 625, 10), ("radix-9", [9, 9], 81, 9), ("radix-9", [9] * 3, 729, 13),
+             ("radix-15", [15, 15], 225, 18), ("radix-15", [15] * 3, 3375, 25)]
+    t3 = []
+    for meth, stp, kk, paper_ms in rows3:
+        fl = P.NSERIES_ALLOW_APPROX if 15 in stp else 0
+        plan3 = P.nseries_plan_finalize(stp, kk, fl)
+        ms3 = _time_evals(lambda: P.nseries_eval(h, A3t, 500, kk, plan=plan3, S=S3, flags=fl, stream=stream), 50, 5,
+                          stream)
+        Sn = S3.cpu().numpy()
+        res = float(np.linalg.norm(np.eye(500) - Sn + A3 @ Sn))
+        t3.append({"method": meth, "k": kk, "products": plan3.products, "ms": ms3, "paper_cpu_ms": paper_ms,
+                   "normal_residual": res})
+    out["paper_table3_d500_fp64"] = t3
+    del A3t, S3
     # NEXT-3 row-sharded chain, config 5 in 8 row blocks, all on this GPU (device-copy gathers):
     # the per-rank kernels of an 8-GPU run (1024 x 8192 x 8192 GEMMs) executed back to back
     n = 8
