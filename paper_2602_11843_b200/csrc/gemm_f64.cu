@@ -331,8 +331,9 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   bool v2 = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
   for (int i = 0; i < ep.n_aux; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.aux[i]) % 16 == 0;
   for (int i = 0; i < ep.n_out; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.out[i]) % 16 == 0;
-  // Tile choice by modelled efficiency: 128x128 (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs
-  // (NSERIES_F64_TILE = 1 / 3 forces one, harness only).
+  // Tile choice: 32x32 for small whole matrices (below), else by modelled efficiency 128x128
+  // (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs (NSERIES_F64_TILE = 1 / 3 / 4 forces one,
+  // harness only).
   if (ep.sym && ep.rows > 0 && ep.rows != d) return (int)cudaErrorInvalidValue;
   const int M = ep.rows > 0 ? ep.rows : d;
   const double nb = std::ceil(d / 128.0), ns = std::ceil(d / 64.0);
@@ -348,6 +349,15 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   else if (ts > 148) es = (ts / 148.0) / (2.0 * std::ceil(ts / 296.0) / 0.87);
   else es = 0.73 * ts / 148.0;
   static const int force = std::getenv("NSERIES_F64_TILE") ? std::atoi(std::getenv("NSERIES_F64_TILE")) : 0;
+  // 32x32 tiles (4 warps of 16x16, several CTAs per SM) win for whole matrices up to d ~ 1470
+  // except where 64x64 tiles fill exactly one wave (d ~ 768: 144 tiles): measured
+  // (`profiles/r01_f64_tile_choice.txt`) 0.27 -> 0.46 of peak at d = 500, 0.72 -> 0.75 at 1024
+  const bool small32 = !ep.sym && M == d && d <= 1472 && !(d > 704 && d <= 800);
+  if (force == 4 || (force == 0 && small32)) {
+    if (ep.sym) return (int)cudaErrorInvalidValue;
+    return v2 ? launch_cfg_t<32, 32, 16, 16, 16, 4, true, false>(X, Y, d, ep, s)
+              : launch_cfg_t<32, 32, 16, 16, 16, 4, false, false>(X, Y, d, ep, s);
+  }
   if (force == 1 || (force == 0 && eb >= es)) {
     return v2 ? launch_cfg<128, 128, 32, 64, 32, 3, true>(X, Y, d, ep, s)
               : launch_cfg<128, 128, 32, 64, 32, 3, false>(X, Y, d, ep, s);

@@ -13,7 +13,7 @@ h = P.nseries_create(0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 out = {"tile": os.environ.get("NSERIES_F64_TILE", "0")}
 g = torch.Generator(device="cuda").manual_seed(0)
-for d in (768, 1024, 1536, 2048, 3072, 4096):
+for d in [int(x) for x in os.environ.get("TILE_D", "768,1024,1536,2048,3072,4096").split(",")]:
     X = torch.randn(d, d, device="cuda", dtype=torch.float64, generator=g)
     Y = torch.randn(d, d, device="cuda", dtype=torch.float64, generator=g)
     C = torch.empty_like(X)
