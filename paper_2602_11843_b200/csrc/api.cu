@@ -97,8 +97,15 @@ nseries_status ensure_ws(nseries_ctx* h, size_t bytes) {
 }
 
 // split-K workspace of the fp32 engine at size d (counters zeroed; the kernel re-zeroes them)
+// largest d for the small-grid fp32 variant (NSERIES_TF32_SMALL_MAXD overrides, harness only)
+int tf32_small_maxd() {
+  static const int v = std::getenv("NSERIES_TF32_SMALL_MAXD") ? std::atoi(std::getenv("NSERIES_TF32_SMALL_MAXD"))
+                                                              : kTf32SmallGridMaxD;
+  return v;
+}
+
 nseries_status ensure_splitk(nseries_ctx* h, int d) {
-  const size_t bytes = tf32_splitk_ws_bytes(d);
+  const size_t bytes = std::max(tf32_splitk_ws_bytes(d), tf32_splitk_ws_bytes_b128(d));
   if (bytes == 0 || bytes <= h->sk_bytes) return NSERIES_OK;
   if (h->sk_ws) {
     cudaDeviceSynchronize();
@@ -259,7 +266,9 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
     int rc;
     if (op.gemm) {
       const int l = lr[i].first, r = lr[i].second;
-      rc = launch_gemm_tf32x3(hi(l), lo(l), hiT(r), loT(r), d, ldp, ep, s, h->sk_ws);
+      rc = (!sym && d <= tf32_small_maxd())
+               ? launch_gemm_tf32x3_b128(hi(l), lo(l), hiT(r), loT(r), d, ldp, ep, s, h->sk_ws)
+               : launch_gemm_tf32x3(hi(l), lo(l), hiT(r), loT(r), d, ldp, ep, s, h->sk_ws);
     } else {
       rc = launch_axpby_f32(d, ep, s);
     }
@@ -1199,7 +1208,10 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
     e32.out_x[0] = static_cast<float*>(C);
     e32.out_ld[0] = d;
     e32.alpha[0] = 1.f;
-    if (!rc) rc = launch_gemm_tf32x3(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream, h->sk_ws);
+    if (!rc)
+      rc = d <= tf32_small_maxd()
+               ? launch_gemm_tf32x3_b128(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream, h->sk_ws)
+               : launch_gemm_tf32x3(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream, h->sk_ws);
     launches = 3;
   }
   h->stats = nseries_stats{};

@@ -34,6 +34,13 @@
 
 #include "internal.h"
 
+// A second translation unit (gemm_tf32_b128.cu) compiles this file again with another tile
+// configuration: NSERIES_TF32_API renames its entry points, NSERIES_TF32_VARIANT drops the
+// configuration-independent kernels (plane split, axpby) from it.
+#ifndef NSERIES_TF32_API
+#define NSERIES_TF32_API(name) name
+#endif
+
 namespace nseries {
 namespace {
 
@@ -889,6 +896,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   }
 }
 
+#ifndef NSERIES_TF32_VARIANT
 // split x (ld_in) into tf32 planes hi/lo and/or transposed planes hiT/loT (ld_out);
 // identity != 0 splits I instead of x.  32x32 tiles through shared memory keep both the
 // row-major and the transposed writes coalesced.
@@ -941,6 +949,8 @@ __global__ void axpby_f32_kernel(int d, const __grid_constant__ EpiParamsF32 ep)
     }
   }
 }
+
+#endif  // NSERIES_TF32_VARIANT
 
 // ---------------------------------------------------------------- host: tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -1038,7 +1048,7 @@ size_t splitk_cnt_bytes(size_t) { return kSplitCntBytes; }
 
 }  // namespace
 
-size_t tf32_splitk_ws_bytes(int d) {
+size_t NSERIES_TF32_API(tf32_splitk_ws_bytes)(int d) {
   int first, S;
   splitk_plan(d, false, &first, &S);
   if (S < 2) return 0;
@@ -1048,8 +1058,8 @@ size_t tf32_splitk_ws_bytes(int d) {
   return splitk_cnt_bytes(tiles) + tiles * (size_t)(BN * BM) * sizeof(float);
 }
 
-int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
-                       const EpiParamsF32& ep_in, void* stream, void* sk_ws) {
+int NSERIES_TF32_API(launch_gemm_tf32x3)(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d,
+                                         int ldp, const EpiParamsF32& ep_in, void* stream, void* sk_ws) {
   EpiParamsF32 ep = ep_in;
   ep.sk_first = 0;
   ep.sk_split = 1;
@@ -1086,6 +1096,7 @@ int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const 
   return (int)cudaGetLastError();
 }
 
+#ifndef NSERIES_TF32_VARIANT
 int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT, float* loT, int ld_out,
                      int d, bool identity, void* stream) {
   const int tiles = (d + 31) / 32;
@@ -1101,5 +1112,7 @@ int launch_axpby_f32(int d, const EpiParamsF32& ep, void* stream) {
   axpby_f32_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(d, ep);
   return (int)cudaGetLastError();
 }
+
+#endif  // NSERIES_TF32_VARIANT
 
 }  // namespace nseries

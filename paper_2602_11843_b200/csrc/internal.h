@@ -190,6 +190,11 @@ struct EpiParamsF32 {
 // bytes of split-K workspace launch_gemm_tf32x3 may use at size d (0: never splits); the first
 // 256 bytes hold counters that must be zero before the first launch (the kernel re-zeroes them)
 size_t tf32_splitk_ws_bytes(int d);
+// the 128x128-tile variant (gemm_tf32_b128.cu) for small grids; same contract
+size_t tf32_splitk_ws_bytes_b128(int d);
+int launch_gemm_tf32x3_b128(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
+                            const EpiParamsF32& ep, void* stream, void* sk_ws = nullptr);
+constexpr int kTf32SmallGridMaxD = 1600;   // api.cu: d <= this (and not symmetric) uses the variant
 int launch_gemm_tf32x3(const float* Xh, const float* Xl, const float* Yh, const float* Yl, int d, int ldp,
                        const EpiParamsF32& ep, void* stream, void* sk_ws = nullptr);
 int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT, float* loT, int ld_out,
