@@ -352,7 +352,8 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   // 32x32 tiles (4 warps of 16x16, several CTAs per SM) win for whole matrices up to d ~ 1470
   // except where 64x64 tiles fill exactly one wave (d ~ 768: 144 tiles): measured
   // (`profiles/r01_f64_tile_choice.txt`) 0.27 -> 0.46 of peak at d = 500, 0.72 -> 0.75 at 1024
-  const bool small32 = !ep.sym && M == d && d <= 1472 && !(d > 704 && d <= 800);
+  // (row blocks of the sharded chain: same rule on the block's M x d area)
+  const bool small32 = !ep.sym && (double)M * d <= 1472.0 * 1472.0 && !(M == d && d > 704 && d <= 800);
   if (force == 4 || (force == 0 && small32)) {
     if (ep.sym) return (int)cudaErrorInvalidValue;
     return v2 ? launch_cfg_t<32, 32, 16, 16, 16, 4, true, false>(X, Y, d, ep, s)
