@@ -207,17 +207,28 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
     const int row = m0 + wm0 + i * 8 + g;
     if (row >= M) continue;
     const int grow = row + ep.row0;   // global row (identity terms)
+    // the row block's aux values are all loaded before its first store: one memory round trip
+    // per row block instead of one per 8x8 block (an output may overwrite its own aux element
+    // in place, which is why the compiler cannot hoist the loads itself)
+    double2 avb[V2 ? C::kNI : 1][kMaxAux];
+    if constexpr (V2) {
+#pragma unroll
+      for (int j = 0; j < C::kNI; ++j) {
+        const int col = n0 + wn0 + j * 8 + 2 * t;
+#pragma unroll
+        for (int x = 0; x < kMaxAux; ++x)
+          if (x < n_aux && col < d)
+            avb[j][x] = *reinterpret_cast<const double2*>(static_cast<const double*>(ep.aux[x]) +
+                                                          (size_t)row * d + col);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < C::kNI; ++j) {
       const int col = n0 + wn0 + j * 8 + 2 * t;
       if (col >= d) continue;
       const size_t off = (size_t)row * d + col;
       if constexpr (V2) {
-        double2 av[kMaxAux];
-#pragma unroll
-        for (int x = 0; x < kMaxAux; ++x)
-          if (x < n_aux) av[x] = *reinterpret_cast<const double2*>(
-                             static_cast<const double*>(ep.aux[x]) + off);
+        const double2 (&av)[kMaxAux] = avb[j];
 #pragma unroll
         for (int o = 0; o < kMaxOut; ++o) {
           if (o >= n_out) break;
