@@ -78,6 +78,10 @@ static_assert(!TWO_SM || CL == 2, "2-SM UMMA needs CTA pairs");
 #define NSERIES_TF32_PREFETCH 0   // (8 measured 19% slower at d = 4096: extra L2 traffic)
 #endif
 constexpr int kPrefetchKB = NSERIES_TF32_PREFETCH;   // L2 prefetch distance (k-blocks) of the producer
+#ifndef NSERIES_TF32_RASTER
+#define NSERIES_TF32_RASTER 8   // pair rows per raster band (1: row-major tile order)
+#endif
+constexpr int kRasterGroup = NSERIES_TF32_RASTER;
 // BK = 16 fp32 = 64-byte rows -> SWIZZLE_64B tiles (8-row atoms of 512 B).  Each 16-wide K
 // chunk is one accumulation unit; NBUF = 4 chunk accumulators keep 4 chunks (24 MMAs) queued
 // ahead of the drain round trip (commit -> epilogue tcgen05.ld -> arrive), which a 2-deep
@@ -535,6 +539,15 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     m0 = (pr * CL + rank) * BM;
     n0 = tn * BN;
     diag_pair = tn == pr;
+  } else if (kRasterGroup > 1) {
+    // grouped raster: bands of kRasterGroup pair rows, column-major inside a band, so the
+    // concurrently resident tiles share their X and Y^T panels in L2
+    const int npr = ((d + BM - 1) / BM + CL - 1) / CL;
+    const int band = kRasterGroup * ntn;
+    const int first = (pair / band) * kRasterGroup;
+    const int gsz = min(npr - first, kRasterGroup);
+    m0 = ((first + (pair % band) % gsz) * CL + rank) * BM;
+    n0 = ((pair % band) / gsz) * BN;
   } else {
     m0 = ((pair / ntn) * CL + rank) * BM;
     n0 = (pair % ntn) * BN;
