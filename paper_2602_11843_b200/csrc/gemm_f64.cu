@@ -73,7 +73,10 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
   double* sB = smem + STAGES * C::kStageA;
 
   // ---- grouped raster: GROUP tile-rows per band
-  constexpr int GROUP = 8;
+#ifndef NSERIES_F64_GROUP
+#define NSERIES_F64_GROUP 8
+#endif
+  constexpr int GROUP = NSERIES_F64_GROUP;
   const int M = ep.rows > 0 ? ep.rows : d;   // rows of X / aux / outputs (row-sharded chain)
   const int ntm = (M + BM - 1) / BM, ntn = (d + BN - 1) / BN;
   const int pid = blockIdx.x;
