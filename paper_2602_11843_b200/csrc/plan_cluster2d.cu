@@ -47,6 +47,10 @@ __device__ __forceinline__ void cp8(double* smem, const double* g, bool ok) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(ok ? 8 : 0));
 }
+__device__ __forceinline__ void cp16(double* smem, const double* g, bool ok) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(ok ? 16 : 0));
+}
 
 // row view (RPC x 64): fragment loads read rows g, columns 4s + t -> XOR-swizzle in 4s
 __device__ __forceinline__ int swz_row(int r, int c) { return r * 64 + (c ^ (4 * ((r & 3) ^ ((r & 1) << 1)))); }
@@ -88,6 +92,39 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
   const int mt = warp >> 2, nt = warp & 3;          // this warp's 8 x 8 tile of the 16 x 32 block
   auto row_off = [&](int slot) { return slot * kRowD; };
   auto col_off = [&](int slot) { return col_base + slot * kColD; };
+  // A into its row view (this CTA's rows, all columns) and column view (all rows, its columns),
+  // issued before the op decode so the memory latency overlaps it; column pairs move as one
+  // 16-byte copy when d is even (both swizzles keep (2c, 2c+1) adjacent)
+  {
+    const bool v16 = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    if (prog.a_row >= 0)
+      for (int i = tid; i < kRowD / 2; i += 256) {
+        const int rl = i >> 5, c = 2 * (i & 31), r = r0 + rl;
+        double* dst = smc + row_off(prog.a_row) + swz_row(rl, c);
+        if (v16) {
+          const bool ok = r < d && c < d;
+          cp16(dst, ok ? A + (size_t)r * d + c : A, ok);
+        } else {   // out-of-range elements are zero-filled from a valid dummy address
+          const bool ok0 = r < d && c < d, ok1 = r < d && c + 1 < d;
+          cp8(dst, ok0 ? A + (size_t)r * d + c : A, ok0);
+          cp8(dst + 1, ok1 ? A + (size_t)r * d + c + 1 : A, ok1);
+        }
+      }
+    if (prog.a_col >= 0)
+      for (int i = tid; i < kColD / 2; i += 256) {
+        const int r = i / (CPC / 2), cl = 2 * (i % (CPC / 2)), c = c0 + cl;
+        double* dst = smc + col_off(prog.a_col) + swz_col(r, cl);
+        if (v16) {
+          const bool ok = r < d && c < d;
+          cp16(dst, ok ? A + (size_t)r * d + c : A, ok);
+        } else {   // out-of-range elements are zero-filled from a valid dummy address
+          const bool ok0 = r < d && c < d, ok1 = r < d && c + 1 < d;
+          cp8(dst, ok0 ? A + (size_t)r * d + c : A, ok0);
+          cp8(dst + 1, ok1 ? A + (size_t)r * d + c + 1 : A, ok1);
+        }
+      }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   for (int i = tid; i < n_ops; i += 256) {
     const C2Op& w = prog.ops[i];
     C2Dev o;
@@ -134,20 +171,7 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // A into its row view (this CTA's rows, all columns) and column view (all rows, its columns)
-  if (prog.a_row >= 0)
-    for (int i = tid; i < kRowD; i += 256) {
-      const int rl = i >> 6, c = i & 63, r = r0 + rl;
-      const bool ok = r < d && c < d;
-      cp8(smc + row_off(prog.a_row) + swz_row(rl, c), ok ? A + (size_t)r * d + c : A, ok);
-    }
-  if (prog.a_col >= 0)
-    for (int i = tid; i < kColD; i += 256) {
-      const int r = i / CPC, cl = i % CPC, c = c0 + cl;
-      const bool ok = r < d && c < d;
-      cp8(smc + col_off(prog.a_col) + swz_col(r, cl), ok ? A + (size_t)r * d + c : A, ok);
-    }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // A (issued first, below)
   uint32_t rpeer[CB], cpeer[RB];            // shared::cluster base of the row / column peers
   {
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smc));
