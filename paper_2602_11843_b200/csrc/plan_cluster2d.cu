@@ -288,10 +288,14 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
     if (tid == 0 && rank == 0) g_c2_prof[3 + 3 * o] = clock64();
 #endif
   }
-  // no CTA leaves while pushes into it are in flight
+  // no CTA leaves while pushes into it are in flight: every byte addressed to this CTA has
+  // landed once all its mbarriers completed, and nothing else touches a peer's shared memory
+  // (st.async carries register values), so no closing cluster barrier is needed
   for (int o = 0; o < n_ops; ++o)
     if (sops[o].tx) wait_bar(o);
+#ifdef NSERIES_C2_END_SYNC
   cluster.sync();
+#endif
 }
 
 template <int RB, int CB>
