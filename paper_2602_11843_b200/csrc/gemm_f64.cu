@@ -340,6 +340,12 @@ int launch_cfg(const double* X, const double* Y, int d, const EpiParams& ep, cud
 
 }  // namespace
 
+#ifndef NSERIES_F64_BK64
+#define NSERIES_F64_BK64 16   // k-tile and stages of the 64x64 configuration
+#define NSERIES_F64_ST64 4
+#endif
+constexpr int kBK64 = NSERIES_F64_BK64, kST64 = NSERIES_F64_ST64;
+
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   bool v2 = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
@@ -377,8 +383,8 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
     return v2 ? launch_cfg<128, 128, 32, 64, 32, 3, true>(X, Y, d, ep, s)
               : launch_cfg<128, 128, 32, 64, 32, 3, false>(X, Y, d, ep, s);
   }
-  return v2 ? launch_cfg<64, 64, 16, 32, 16, 4, true>(X, Y, d, ep, s)
-            : launch_cfg<64, 64, 16, 32, 16, 4, false>(X, Y, d, ep, s);
+  return v2 ? launch_cfg<64, 64, kBK64, 32, 16, kST64, true>(X, Y, d, ep, s)
+            : launch_cfg<64, 64, kBK64, 32, 16, kST64, false>(X, Y, d, ep, s);
 }
 
 int launch_axpby_f64(int d, const EpiParams& ep, void* stream) {
