@@ -483,3 +483,24 @@ def test_table3_on_gpu(h, steps, printed):
         assert float(f"{res:.1e}") == printed, res
     else:
         assert res <= 1e-12, res
+
+
+def test_host_api_async_size_changes(h):
+    # NSERIES_HOST_ASYNC calls of growing and shrinking d on one handle: the staging sets are
+    # re-allocated (after draining the pipeline) when a larger matrix arrives; every result is
+    # the synchronous call's
+    steps = [5, 2]
+    k = OP.plan_reaches(steps)
+    plan = P.nseries_plan_finalize(steps, k, 0)
+    mats, outs = [], []
+    for i, d in enumerate([40, 300, 70, 520, 300]):
+        a = torch.from_numpy(inputs.random_matrix(d, 60 + i, 0.7)).pin_memory()
+        s_ = torch.full_like(a, float("nan")).pin_memory()
+        P.nseries_eval_host(h, a, d, k, plan=plan, S=s_, flags=P.NSERIES_HOST_ASYNC)
+        mats.append(a)
+        outs.append(s_)
+    P.nseries_host_sync(h)
+    for a, s_ in zip(mats, outs):
+        ref = torch.empty_like(a)
+        P.nseries_eval_host(h, a, a.shape[0], k, plan=plan, S=ref)
+        assert torch.equal(s_, ref)
