@@ -465,10 +465,10 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     if (tid == 0 && rank == 0) g_small_prof[3 + 3 * o] = clock64();
 #endif
   }
-  // no CTA leaves while pushes into it are in flight
+  // no CTA leaves while pushes into it are in flight (every byte addressed to it has landed once
+  // its mbarriers completed; st.async carries register values: no closing cluster barrier)
   for (int o = 0; o < n_ops; ++o)
     if (sops[o].push) wait_bar(o);
-  cluster.sync();
 }
 
 template <int NC>
