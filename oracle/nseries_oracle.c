@@ -28,6 +28,9 @@
  *                      by its monomial coefficients and applied by Horner in
  *                      R_n.  "+1" steps (no paper counterpart; DESIGN.md
  *                      reading R5) are Y' = Y + R, R' = A R.
+ *   or_series_sum_batch -- C-1 for a batch of small independent matrices
+ *                      (config 4): the same Horner sum per matrix, OpenMP
+ *                      over matrices instead of rows.
  *   or_matvec       -- W = X V in long double (used to form S_gpu V on the
  *                      host for probe-mode parity).
  *
@@ -85,20 +88,6 @@ int or_num_threads(void) {
 int or_matvec(const double* X, int d, const ld* V, int p, ld* W) {
   if (d < 1 || p < 1 || !X || !V || !W) return 1;
   matvec_block(X, d, V, p, W);
-  return 0;
-}
-
-/* Same, for a long double matrix X (used for S_gpu V when S_gpu has been widened). */
-int or_matvec_ld(const ld* X, int d, const ld* V, int p, ld* W) {
-  if (d < 1 || p < 1 || !X || !V || !W) return 1;
-#pragma omp parallel for schedule(static)
-  for (int i = 0; i < d; ++i) {
-    for (int c = 0; c < p; ++c) {
-      ld acc = 0.0L;
-      for (int j = 0; j < d; ++j) acc += X[(size_t)i * d + j] * V[(size_t)j * p + c];
-      W[(size_t)i * p + c] = acc;
-    }
-  }
   return 0;
 }
 
@@ -213,4 +202,48 @@ int or_plan_apply(const double* A, int d, int n_steps, const int* kind, const in
   apply_Y(&P, n_steps, V, Y_out);
   if (R_out) apply_R(&P, n_steps, V, R_out);
   return 0;
+}
+
+/*
+ * C-1 for `batch` independent matrices (config 4's batched small path):
+ *   out_b[d][p] = sum_{j=0}^{k-1} A_b^j V_b, b = 0..batch-1,
+ * A_b at A + b*d*d (binary64), V_b / out_b at V / out + b*d*p (long double).
+ * Per matrix the plain power sum of or_series_sum (w <- A w,
+ * out += w) with the plain left-to-right dot product; the parallel loop runs
+ * over matrices, so the result of each matrix does not depend on threads.
+ */
+int or_series_sum_batch(const double* A, int batch, int d, int64_t k, const ld* V, int p, ld* out) {
+  if (batch < 0 || d < 1 || p < 1 || k < 1 || (batch > 0 && (!A || !V || !out))) return 1;
+  const size_t n = (size_t)d * p;
+  int bad = 0;
+#pragma omp parallel
+  {
+    ld* w = (ld*)malloc(n * sizeof(ld));
+    ld* w2 = (ld*)malloc(n * sizeof(ld));
+    if (!w || !w2) {
+#pragma omp atomic write
+      bad = 2;
+    }
+#pragma omp for schedule(dynamic, 16)
+    for (int b = 0; b < batch; ++b) {
+      if (!w || !w2) continue;
+      const double* Ab = A + (size_t)b * d * d;
+      ld* ob = out + (size_t)b * n;
+      memcpy(w, V + (size_t)b * n, n * sizeof(ld));
+      memcpy(ob, w, n * sizeof(ld));
+      for (int64_t j = 1; j < k; ++j) {
+        for (int i = 0; i < d; ++i)
+          for (int c = 0; c < p; ++c) {
+            ld acc = 0.0L;
+            for (int q = 0; q < d; ++q) acc += (ld)Ab[(size_t)i * d + q] * w[(size_t)q * p + c];
+            w2[(size_t)i * p + c] = acc;
+          }
+        ld* t = w; w = w2; w2 = t;
+        for (size_t i = 0; i < n; ++i) ob[i] += w[i];
+      }
+    }
+    free(w);
+    free(w2);
+  }
+  return bad;
 }

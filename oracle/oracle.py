@@ -5,6 +5,7 @@ this module.  It builds and loads oracle/liboracle.so (oracle/nseries_oracle.c)
 and exposes:
 
   series_sum(A, k, V)          C-1: S_k(A) V = sum_{j<k} A^j V
+  series_sum_batch(Ab, k, Vb)  C-1 per matrix of a batch (config 4)
   plan_apply(A, steps, V)      C-2: Y_n V (and R_n V) of a radix plan
   full_series(A, k)            C-1 with V = I (small d)
   kernel_coeff_vectors(...)    [f]_j per step, exact rationals -> long double
@@ -37,8 +38,10 @@ _i_p = ctypes.POINTER(ctypes.c_int)
 def build(force=False):
     """Compile the C oracle (gcc, OpenMP, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
-        subprocess.check_call(cmd)
+        tmp = _LIB + ".%d.tmp" % os.getpid()       # built aside, then renamed: a process that
+        cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"]   # has the old
+        subprocess.check_call(cmd)                                                   # .so keeps it
+        os.replace(tmp, _LIB)
     return _LIB
 
 
@@ -54,6 +57,9 @@ def lib():
         L.or_plan_apply.argtypes = [_d_p, ctypes.c_int, ctypes.c_int, _i_p, _i_p, _i_p, _ld_p,
                                     _ld_p, ctypes.c_int, _ld_p, _ld_p]
         L.or_plan_apply.restype = ctypes.c_int
+        L.or_series_sum_batch.argtypes = [_d_p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _ld_p,
+                                          ctypes.c_int, _ld_p]
+        L.or_series_sum_batch.restype = ctypes.c_int
         L.or_matvec.argtypes = [_d_p, ctypes.c_int, _ld_p, ctypes.c_int, _ld_p]
         L.or_matvec.restype = ctypes.c_int
         L.or_num_threads.argtypes = []
@@ -104,6 +110,26 @@ def series_sum(A, k, V, norm_bound=None, tail_tol=0.0):
     if rc != 0:
         raise RuntimeError(f"or_series_sum failed rc={rc}")
     return out, int(used.value)
+
+
+def series_sum_batch(Ab, k, Vb):
+    """C-1 per matrix of a batch: out[b] = sum_{j<k} A_b^j V_b in long double.
+    Ab: (batch, d, d) float64/float32 (widened exactly); Vb: (batch, d, p)."""
+    Ab = np.asarray(Ab)
+    if Ab.dtype == np.float32:
+        Ab = Ab.astype(np.float64)
+    Ab = np.ascontiguousarray(Ab, dtype=np.float64)
+    batch, d, _ = Ab.shape
+    Vb = np.ascontiguousarray(np.asarray(Vb).astype(LD))
+    if Vb.shape[:2] != (batch, d):
+        raise ValueError("Vb must be (batch, d, p)")
+    p = Vb.shape[2]
+    out = np.empty((batch, d, p), dtype=LD)
+    rc = lib().or_series_sum_batch(Ab.ctypes.data_as(_d_p), batch, d, int(k), Vb.ctypes.data_as(_ld_p), p,
+                                   out.ctypes.data_as(_ld_p))
+    if rc != 0:
+        raise RuntimeError(f"or_series_sum_batch failed rc={rc}")
+    return out
 
 
 def full_series(A, k):

@@ -44,9 +44,8 @@ struct nseries_ctx {
   cudaStream_t cap_stream = nullptr;
   struct CachedGraph { cudaGraphExec_t exec; int launches; };
   std::map<std::string, CachedGraph> graphs;
-  // small fp64 single-matrix kernels (d <= 64), tried in order: 2-D cluster, 1-D cluster,
-  // single-CTA shared memory, single-CTA global slots.  NSERIES_SMALL_MODE selects the first
-  // one tried: 0 (2-D cluster, default), 3 (1-D cluster), 1 (shared memory), 2 (global)
+  // small fp64 single matrices (d <= 64): 0 = one launch of the 4 x 2 cluster kernel when the
+  // plan fits (default), 1 = tiled engine (NSERIES_SMALL_MODE, for tests)
   int small_mode = 0;
   // fp32 engine split-K workspace (tail-wave partial accumulators + per-tile counters)
   void* sk_ws = nullptr;
@@ -326,11 +325,12 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
 }
 
 // Execute a compiled program on the stream.  fp64 with d <= 64: the whole op list runs in one
-// single-CTA launch (plan_small.cu); otherwise one tiled GEMM launch per op.
+// launch of the 4 x 2 cluster kernel (plan_cluster2d.cu) when its live set fits shared memory;
+// otherwise (and with NSERIES_SMALL_MODE=1) one tiled GEMM launch per op.
 nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void* S, void* R,
                            int d, nseries_dtype dt, cudaStream_t s, int* launches, bool sym = false) {
   if (dt != NSERIES_F64) return NSERIES_ERR_INVALID_ARG;
-  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && h->small_mode == 0) {
+  if (h->small_mode == 0 && cluster2d_fits(P, d)) {
     // 4 x 2 cluster, each CTA a 16 x 32 block of every product (row / column views, DSMEM pushes)
     auto c2 = std::make_unique<C2Program>();   // ~8 KB: heap, copied into the launch parameters
     if (build_cluster2d_program(P, c2.get()) == NSERIES_OK) {
@@ -343,69 +343,6 @@ nseries_status run_program(nseries_ctx* h, const Program& P, const void* A, void
       }
       if (rc != -1) return cuda_fail(h, (cudaError_t)rc);
     }
-  }
-  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && (h->small_mode == 0 || h->small_mode == 3)) {
-    // 8-CTA cluster, each CTA an 8-row block of every value (right factors replicated)
-    WarpProgram wp{};
-    if (build_cluster_program(P, &wp) == NSERIES_OK) {
-      const int rc = launch_plan_cluster_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
-                                             static_cast<double*>(R), s);
-      if (rc == 0) {
-        if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
-        *launches = 1;
-        return NSERIES_OK;
-      }
-      if (rc != -1) return cuda_fail(h, (cudaError_t)rc);
-    }
-  }
-  if (d <= 64 && (int)P.ops.size() <= kMaxBatchedOps && (h->small_mode <= 1 || h->small_mode == 3)) {
-    // whole plan with every value in shared memory (falls through if the live set is too big)
-    WarpProgram wp{};
-    if (build_warp_program(P, &wp) == NSERIES_OK) {
-      const int rc = launch_plan_smem_f64(d, wp, static_cast<const double*>(A), static_cast<double*>(S),
-                                          static_cast<double*>(R), s);
-      if (rc == 0) {
-        if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
-        *launches = 1;
-        return NSERIES_OK;
-      }
-      if (rc != -1) return cuda_fail(h, (cudaError_t)rc);
-    }
-  }
-  if (d <= 64 && (int)P.ops.size() <= kMaxSmallOps) {
-    const size_t slot = (size_t)d * d * sizeof(double);
-    auto ptr = [&](int v) -> double* {
-      switch (P.val_kind[v]) {
-        case V_USER_A: return const_cast<double*>(static_cast<const double*>(A));
-        case V_IDENT: return static_cast<double*>(h->ident);
-        case V_USER_S: return static_cast<double*>(S);
-        case V_USER_R: return static_cast<double*>(R);
-        default: return reinterpret_cast<double*>(static_cast<char*>(h->ws) + (size_t)P.val_buf[v] * slot);
-      }
-    };
-    SmallProgram sp{};
-    sp.n_ops = (int)P.ops.size();
-    for (int i = 0; i < sp.n_ops; ++i) {
-      const Op& op = P.ops[i];
-      SmallOp& so = sp.ops[i];
-      so.gemm = op.gemm ? 1 : 0;
-      so.X = op.gemm ? ptr(op.X) : nullptr;
-      so.Y = op.gemm ? ptr(op.Y) : nullptr;
-      so.n_aux = op.n_aux;
-      so.n_out = op.n_out;
-      for (int a = 0; a < op.n_aux; ++a) so.aux[a] = ptr(op.aux[a]);
-      for (int j = 0; j < op.n_out; ++j) {
-        so.out[j] = ptr(op.out[j]);
-        so.alpha[j] = op.alpha[j];
-        so.gamma[j] = op.gamma[j];
-        for (int a = 0; a < kMaxAux; ++a) so.beta[j][a] = op.beta[j][a];
-      }
-    }
-    const int rc = launch_plan_small_f64(d, sp, s);
-    if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
-    if (h->want_ev_S) cudaEventRecordWithFlags(h->ev_S, s, cudaEventRecordExternal);
-    *launches = 1;
-    return NSERIES_OK;
   }
   return run_program_range(h, P, A, S, R, d, s, 0, (int)P.ops.size(), launches, -1, -1, nullptr, sym);
 }
@@ -800,7 +737,9 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   st = ensure_ws(h, dt == NSERIES_F64 ? (size_t)P.n_slots * d * d * sizeof(double) : f32_ws_bytes(P, d));
   if (st == NSERIES_OK && dt == NSERIES_F32) st = ensure_splitk(h, d);
   if (st != NSERIES_OK) return st;
-  if (P.needs_identity) {
+  // the 4 x 2 cluster kernel (fp64, d <= 64) synthesises I in its fragments: no identity buffer
+  const bool one_launch = dt == NSERIES_F64 && h->small_mode == 0 && cluster2d_fits(P, d);
+  if (P.needs_identity && !one_launch) {
     st = ensure_identity(h, d, dt, s);
     if (st != NSERIES_OK) return st;
   }

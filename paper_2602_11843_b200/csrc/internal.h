@@ -202,29 +202,6 @@ int launch_split_f32(const float* x, int ld_in, float* hi, float* lo, float* hiT
 int launch_axpby_f32(int d, const EpiParamsF32& ep, void* stream);
 inline int padded_ld(int d) { return (d + 31) / 32 * 32; }
 
-// Small single-matrix path (plan_small.cu): whole op list in one single-CTA launch, d <= 64.
-constexpr int kMaxSmallOps = 40;
-struct SmallOp {
-  const double* X;
-  const double* Y;
-  const double* aux[kMaxAux];
-  double* out[kMaxOut];
-  double alpha[kMaxOut];
-  double beta[kMaxOut][kMaxAux];
-  double gamma[kMaxOut];
-  int gemm, n_aux, n_out;
-};
-struct SmallProgram {
-  int n_ops;
-  SmallOp ops[kMaxSmallOps];
-};
-int launch_plan_small_f64(int d, const SmallProgram& prog, void* stream);
-// Same, with every value of the plan resident in shared memory (slot codes of WarpProgram,
-// in-place slots); returns -1 if the plan's live set does not fit (caller falls back).
-int launch_plan_smem_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
-// Cluster of 4 CTAs, each holding a 16-row block of every value (operand rows of the other CTAs
-// read through distributed shared memory); prog built with inplace = false.  -1 if unsupported.
-int launch_plan_cluster_f64(int d, const WarpProgram& prog, const double* A, double* S, double* R, void* stream);
 // 2-D cluster kernel (plan_cluster2d.cu): CTA (r, c) of an RB x CB cluster owns the 64/RB x
 // 64/CB block (r, c) of every product.  A value read as a LEFT factor lives in "row views"
 // (the CTA's 64/RB rows, all 64 columns, replicated across its row group), one read as a RIGHT
@@ -246,12 +223,9 @@ struct C2Program {
   C2Op ops[kMaxBatchedOps];
 };
 nseries_status build_cluster2d_program(const Program& P, C2Program* out);
+// true if the whole program runs as one 4 x 2 cluster launch at this d (op count, shared memory)
+bool cluster2d_fits(const Program& P, int d);
 int launch_plan_cluster2d_f64(int d, const C2Program& prog, const double* A, double* S, double* R, void* stream);
-
-// Slot layout for the cluster kernel: values read as a right operand live in slots replicated in
-// every CTA (each CTA pushes its rows of such outputs to all peers); the others in per-CTA
-// row-block slots.  No in-place reuse.
-nseries_status build_cluster_program(const Program& P, WarpProgram* wp);
 
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);

@@ -20,6 +20,7 @@
 // value; that holds once the same peer group has pushed again since the old value's last read
 // (the pushes follow the pusher's mainloop).  build_cluster2d_program marks ops where no such
 // push lies in between (`csync`: full cluster barrier before their pushes).
+#include <memory>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -299,11 +300,16 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
 }
 
 template <int RB, int CB>
-int launch_c2(int d, const C2Program& prog, const double* A, double* S, double* R, cudaStream_t stream) {
+size_t c2_smem_bytes(const C2Program& prog) {
   constexpr int RPC = 64 / RB, CPC = 64 / CB;
-  const size_t smem = ((size_t)prog.n_row * RPC * 64 + (size_t)prog.n_col * 64 * CPC + (size_t)prog.n_own * RPC * CPC) *
-                          sizeof(double) +
-                      (size_t)prog.n_ops * (sizeof(C2Dev) + sizeof(uint64_t));
+  return ((size_t)prog.n_row * RPC * 64 + (size_t)prog.n_col * 64 * CPC + (size_t)prog.n_own * RPC * CPC) *
+             sizeof(double) +
+         (size_t)prog.n_ops * (sizeof(C2Dev) + sizeof(uint64_t));
+}
+
+template <int RB, int CB>
+int launch_c2(int d, const C2Program& prog, const double* A, double* S, double* R, cudaStream_t stream) {
+  const size_t smem = c2_smem_bytes<RB, CB>(prog);
   if (smem > 227 * 1024) return -1;
   cudaError_t e = cudaFuncSetAttribute(plan_cluster2d_f64_kernel<RB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
@@ -428,6 +434,13 @@ nseries_status build_cluster2d_program(const Program& P, C2Program* out) {
     }
   }
   return NSERIES_OK;
+}
+
+bool cluster2d_fits(const Program& P, int d) {
+  if (d > 64 || (int)P.ops.size() > kMaxBatchedOps) return false;
+  auto c2 = std::make_unique<C2Program>();
+  if (build_cluster2d_program(P, c2.get()) != NSERIES_OK) return false;
+  return c2_smem_bytes<4, 2>(*c2) <= 227 * 1024;
 }
 
 int launch_plan_cluster2d_f64(int d, const C2Program& prog, const double* A, double* S, double* R, void* stream) {

@@ -14,6 +14,12 @@ differ by rounding; a test always hands the SAME array to both sides.
 """
 from __future__ import annotations
 
+import hashlib
+import os
+import subprocess
+import sys
+import tempfile
+
 import numpy as np
 
 CONFIG_NAMES = {
@@ -129,3 +135,33 @@ def random_matrix(d, seed, scale=0.5):
     """Generic A = scale G / sqrt(d) for parity sweeps."""
     rng = np.random.default_rng(seed)
     return scale * rng.standard_normal((d, d)) / np.sqrt(max(d, 1))
+
+
+# OpenBLAS pinned to one thread and to its Haswell kernels: numpy's QR / GEMM then run the same
+# instruction sequence on any x86-64 host with AVX2, so a CPU-built A has the same bits here and
+# on the GPU box (with 8 threads, or the host's own kernel choice, the bits differ run to run
+# across hosts).  Used for the matrices the committed goldens (tests/golden/) were computed on.
+REPRO_ENV = {"OPENBLAS_CORETYPE": "Haswell", "OPENBLAS_NUM_THREADS": "1", "OMP_NUM_THREADS": "1",
+             "MKL_NUM_THREADS": "1"}
+
+
+def sha256(a):
+    """SHA-256 of an array's bytes (C order) -- identifies the exact A a golden belongs to."""
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def cpu_reproducible(name, full=False, **kw):
+    """inputs.<name>(device="cpu", **kw) computed in a child process under REPRO_ENV; returns A
+    (the first element if the generator returns a tuple), or the whole tuple with full=True.
+    cfg3: ~16 s, cfg5: ~190 s."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "r.npz")
+        code = ("import sys; sys.path.insert(0, %r); import numpy as np; "
+                "from paper_2602_11843_b200 import inputs; r = inputs.%s(**%r); "
+                "r = r if isinstance(r, tuple) else (r,); "
+                "np.savez(%r, *r)" % (root, name, dict(kw), out))
+        subprocess.run([sys.executable, "-c", code], env={**os.environ, **REPRO_ENV}, check=True)
+        z = np.load(out)
+        r = tuple(z["arr_%d" % i] for i in range(len(z.files)))
+        return r if full else r[0]

@@ -254,3 +254,21 @@ def test_plan_radix15_deviation_from_series(oracle_lib):
         W = O.matvec(A, W)
     lhs = (Y - S) - O.matvec(A, np.asarray(Y - S, dtype=np.float64))
     assert O.rel_fro(lhs, W - R) < 1e-6
+
+
+def test_series_sum_batch(oracle_lib):
+    # the batched C-1 entry (config 4) is the same per-matrix power sum: bit-identical to
+    # series_sum on every matrix, and the diagonal closed form per matrix
+    rng = np.random.default_rng(5)
+    batch, d, k = 6, 7, 23
+    Ab = 0.4 * rng.standard_normal((batch, d, d)) / np.sqrt(d)
+    Ab[2] = np.diag(rng.uniform(-0.9, 0.9, d))
+    Vb = rng.standard_normal((batch, d, 3))
+    out = O.series_sum_batch(Ab, k, Vb)
+    for b in range(batch):
+        ref, _ = O.series_sum(Ab[b], k, Vb[b])
+        assert np.array_equal(out[b], ref)
+    a = np.diag(Ab[2]).astype(LD)
+    closed = ((1 - a ** k) / (1 - a))[:, None] * Vb[2].astype(LD)
+    assert O.rel_fro(out[2], closed) <= 1e-17
+    assert O.series_sum_batch(Ab[:0], k, Vb[:0]).shape == (0, d, 3)
