@@ -333,6 +333,7 @@ plan_cluster_f64_kernel(int d, const double* __restrict__ A, double* __restrict_
     c.tx = (NC - 1) * kLSlotD * 8 * __popc(c.push);
     sops[i] = c;
   }
+  __syncthreads();   // every op decoded (threads 0..n_ops-1) before thread 0 reads push / tx
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sops + n_ops);   // one mbarrier per op
   if (tid == 0) {
     int last = -1;

@@ -1,5 +1,7 @@
 """Config 4 timing (harness-only): 16384 x 32x32 fp32 batched, one launch per eval.
-NSERIES_BATCHED_WPM selects warps per matrix (library tuning knob)."""
+NSERIES_BATCHED_WPM selects warps per matrix (library tuning knob); NSERIES_LIB an A/B build.
+Also prints the worst relative Frobenius error over a 512-matrix sample against an fp64 torch
+power-sum reference (sanity for A/B variants; parity lives in tests/)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -9,6 +11,19 @@ h = P.nseries_create(0)
 Ab = torch.from_numpy(inputs.cfg4()).cuda()
 S = torch.empty_like(Ab)
 B, d = Ab.shape[0], Ab.shape[1]
+samp = torch.arange(0, B, B // 512, device="cuda")
+A64 = Ab[samp].double()
+
+
+def ref_series(k):
+    W = torch.eye(d, dtype=torch.float64, device="cuda").expand_as(A64).clone()
+    out = W.clone()
+    for _ in range(k - 1):
+        W = torch.bmm(A64, W)
+        out += W
+    return out
+
+
 for steps, k in (([9, 9], 81), ([5, 5], 25)):
     plan = P.nseries_plan_finalize(steps, k, 0)
     for _ in range(3): P.nseries_eval_batched_strided(h, Ab, d * d, B, d, k, plan=plan, S=S)
@@ -19,7 +34,10 @@ for steps, k in (([9, 9], 81), ([5, 5], 25)):
     for _ in range(n): P.nseries_eval_batched_strided(h, Ab, d * d, B, d, k, plan=plan, S=S)
     e1.record(); torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / n * 1e3
-    print(json.dumps({"wpm": os.environ.get("NSERIES_BATCHED_WPM", "default"), "plan": steps, "k": k,
+    R = ref_series(k)
+    err = ((S[samp].double() - R).flatten(1).norm(dim=1) / R.flatten(1).norm(dim=1)).max().item()
+    print(json.dumps({"lib": os.path.basename(os.environ.get("NSERIES_LIB", "libnseries.so")),
+                      "wpm": os.environ.get("NSERIES_BATCHED_WPM", "default"), "plan": steps, "k": k,
                       "us": round(us, 1), "matrices_per_s": B / us * 1e6,
                       "hbm_gbs": 2 * B * d * d * 4 / us / 1e3,
-                      "tflops_alg": plan.products * 2 * d ** 3 * B / us / 1e6}))
+                      "tflops_alg": plan.products * 2 * d ** 3 * B / us / 1e6, "max_rel_err": err}))
