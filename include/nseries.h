@@ -46,7 +46,7 @@ typedef struct nseries_ctx* nseries_handle;
 typedef enum {
   NSERIES_OK = 0,
   NSERIES_ERR_INVALID_ARG = 1,      /* bad pointer / size / flag combination          */
-  NSERIES_ERR_UNSUPPORTED_RADIX = 2,/* radix outside {2,3,5,9,15} (or "+1" = 1)       */
+  NSERIES_ERR_UNSUPPORTED_RADIX = 2,/* radix outside 2..32 (or "+1" = 1)              */
   NSERIES_ERR_PLAN_K_MISMATCH = 3,  /* plan does not reach k (pure plan with k!=m^t) */
   NSERIES_ERR_APPROX_TELESCOPE = 4, /* approximate kernel in a telescoping-form step,
                                        or approximate radix without ALLOW_APPROX      */
@@ -97,8 +97,12 @@ typedef enum {
 
 #define NSERIES_MAX_STEPS 128
 
-/* A plan: a sequence of steps from n = 1 to n = k.  step[i] = m in {2,3,5,9,15}
- * multiplies n by m; step[i] = 1 is a "+1" step.  form[i] is filled by the
+/* A plan: a sequence of steps from n = 1 to n = k.  step[i] = m in 2..32 multiplies n by m;
+ * step[i] = 1 is a "+1" step.  Kernels: m = 2 binary, 3 ternary, 5 the radix-5 kernel, 9 the
+ * exact radix-9 kernel (Theorem 1), 15 the approximate radix-15 kernel (residual framework);
+ * every other m is naive radix-m splitting: the powers B^2 .. B^{m-1}
+ * (m - 2 products) with T_m = I + B + ... + B^{m-1} accumulated in their epilogues, then the
+ * concatenation and the next power -- C(m) = m products per step.  form[i] is filled by the
  * builder: 0 = telescoping power update R' = I - T + T R (exact kernels,
  * PAPER.md:211-212), 1 = paper residual update R' = I - M Y',
  * 2 = telescoping-form residual R' = I - f + f R.  products = GEMMs executed

@@ -14,6 +14,8 @@ consumes.
 Circuits encoded here, each following the paper's text line by line:
   * T_2 binary:    f = 1 + z
   * T_3 ternary:   U = B^2; T = I + B + U
+  * T_m naive:     P_2 = B^2, P_j = P_{j-1} B; T = I + B + P_2 + ... + P_{m-1}
+                   (m = 4..32 except 5, 9, 15)           PAPER.md:140-151
   * T_5 quinary:   U = B^2; V = U(B+U); T = I+B+U+V
   * T_9 radix-9:   U = B^2; V = U(B+2U); P = 3/20 B + 2U + V;
                    Q = 11/40 B - 1/8 U + 1/4 V; W = PQ;
@@ -99,6 +101,21 @@ def circuit_ternary():
     basis: [I, B, U]."""
     steps = [([0, 1], [0, 1])]                                  # U = B * B
     final = [F(1), F(1), F(1)]
+    return steps, final
+
+
+def circuit_naive(m):
+    """Naive radix-m splitting kernel ("Radix-m splitting"): the powers
+    A^{2n}, ..., A^{(m-1)n} from A^n -- P_2 = B * B, P_j = P_{j-1} * B (m - 2 products) --
+    and T_m = I + B + P_2 + ... + P_{m-1}.  basis: [I, B, P_2, ..., P_{m-1}]."""
+    if m < 3:
+        raise ValueError("naive radix-m needs m >= 3 (m = 2 is binary splitting)")
+    steps = [([0, 1], [0, 1])]                                  # P_2 = B * B
+    for j in range(3, m):
+        left = [0] * j
+        left[j - 1] = 1                                         # P_{j-1} (basis index j - 1)
+        steps.append((left, [0, 1]))                            # P_j = P_{j-1} * B
+    final = [F(1)] * m
     return steps, final
 
 
@@ -202,6 +219,8 @@ def kernel_coeffs(m, variant="polished"):
         steps, final = circuit_binary()
     elif m == 3:
         steps, final = circuit_ternary()
+    elif m in NAIVE:
+        steps, final = circuit_naive(m)
     elif m == 5:
         steps, final = circuit_quinary()
     elif m == 9:
@@ -214,8 +233,11 @@ def kernel_coeffs(m, variant="polished"):
     return eval_circuit(steps, final)
 
 
+# naive radix-m splitting for the other m up to 32: m - 2 products
+NAIVE = tuple(m for m in range(4, 33) if m not in (5, 9, 15))
 MU = {2: 0, 3: 1, 5: 2, 9: 3, 15: 4}    # products per kernel
-EXACT = {2: True, 3: True, 5: True, 9: True, 15: False}
+MU.update({m: m - 2 for m in NAIVE})
+EXACT = {m: m != 15 for m in MU}
 
 
 def circuit_products(m):
@@ -229,4 +251,6 @@ def circuit_products(m):
         return len(circuit_radix9()[0])
     if m == 15:
         return len(circuit_radix15(printed_radix15_fractions())[0])
+    if m in NAIVE:
+        return len(circuit_naive(m)[0])
     raise ValueError(m)

@@ -89,7 +89,12 @@ __device__ void op_f32(const BatchedOp& op, float* slots, int d) {
           for (int i = 0; i < 2; ++i) split_tf32(bf[i], bh[i], bl[i]);
           mma_tf32(small[h], al, bh);
           mma_tf32(small[h], ah, bl);
-          mma_tf32(big[h], ah, bh);
+          // hi*hi of each k-step from a zero accumulator, summed with IEEE adds (a chained
+          // tensor-core accumulator truncates at every k-step; same as batched_warp.cu)
+          float tk[4] = {0.f, 0.f, 0.f, 0.f};
+          mma_tf32(tk, ah, bh);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) big[h][e] += tk[e];
         }
       }
     }

@@ -193,8 +193,27 @@ __device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, 
     for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
       for (int j = 0; j < NBW; ++j) {
+#if defined(NSERIES_BW_CHAIN_BIG)
         if (s == 0) mma_tf32_z(big[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
         else mma_tf32(big[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
+#else
+        // hi*hi of each k-step from a zero accumulator, summed in fp32 registers with IEEE
+        // round-to-nearest adds: a chained tensor-core accumulator truncates at every k-step
+        // (profiles/r01_tf32_accumulation_probe.txt), which biases the dominant term; the
+        // cross terms (2^-11 smaller) stay chained
+        if (s == 0) {
+          mma_tf32_z(big[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
+        } else {
+          float tk[4];
+          mma_tf32_z(tk, ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
+          const unsigned long long p01 = add2(pk(big[mb][j][0], big[mb][j][1]), pk(tk[0], tk[1]));
+          const unsigned long long p23 = add2(pk(big[mb][j][2], big[mb][j][3]), pk(tk[2], tk[3]));
+          big[mb][j][0] = __uint_as_float((uint32_t)p01);
+          big[mb][j][1] = __uint_as_float((uint32_t)(p01 >> 32));
+          big[mb][j][2] = __uint_as_float((uint32_t)p23);
+          big[mb][j][3] = __uint_as_float((uint32_t)(p23 >> 32));
+        }
+#endif
       }
 #pragma unroll
     for (int mb = 0; mb < 2; ++mb)

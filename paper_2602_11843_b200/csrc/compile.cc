@@ -80,7 +80,9 @@ struct Builder {
 nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog) {
   Program& P = *prog;
   P = Program();
-  P.ops.reserve(8 * (size_t)plan.n_steps + 8);   // Op& references stay valid while building
+  size_t n_ops_max = 8;
+  for (int i = 0; i < plan.n_steps; ++i) n_ops_max += (size_t)std::max(kernel_mu(plan.step[i]), 1) + 2;
+  P.ops.reserve(n_ops_max);   // Op& references stay valid while building
   Builder b(P);
   const bool elide = (plan.flags & NSERIES_ELIDE_TRIVIAL) != 0;
   int S = b.ident;   // S_1 = I  (Y_0 = I)
@@ -132,10 +134,20 @@ nseries_status compile_plan(const nseries_plan& plan, bool want_R, Program* prog
     }
     int T = -1;   // kernel value T_m(B) / f(R)
     int f_for_tele = -1;
-    if (m == 3) {
-      // ternary splitting: U = B^2, T_3 = I + B + U
-      Op& g1 = b.gemm(B, B, i, "x3.U");
-      T = b.out(g1, 1.0, {{B, 1.0}}, 1.0);
+    if (m == 3 || (m != 5 && m != 9 && m != 15 && kernel_mu(m) == m - 2)) {
+      // ternary and naive radix-m splitting: the powers
+      // B^2 = B B, B^j = B^{j-1} B (m - 2 products), T_m = I + B + ... + B^{m-1} accumulated
+      // in the same epilogues (T_j = T_{j-1} + B^j); concatenation and next power below
+      Op& g1 = b.gemm(B, B, i, m == 3 ? "x3.U" : "xm.P2");
+      int Tacc = b.out(g1, 1.0, {{B, 1.0}}, 1.0);           // I + B + B^2
+      int Pj = m > 3 ? b.out(g1, 1.0, {}) : -1;             // B^2
+      for (int j = 3; j < m; ++j) {
+        Op& gj = b.gemm(Pj, B, i, "xm.Pj");                   // acc = B^j
+        const int Tn = b.out(gj, 1.0, {{Tacc, 1.0}});
+        Pj = j + 1 < m ? b.out(gj, 1.0, {}) : -1;
+        Tacc = Tn;
+      }
+      T = Tacc;
     } else if (m == 5) {
       // quinary (Eqs. quinary-U/V/final 866-873)
       Op& g1 = b.gemm(B, B, i, "x5.U");

@@ -19,6 +19,7 @@ struct Radix15Params {
   double L2[3], R2[3], L3[4], R3[4], L4[5], R4[5], gamma[4];
 };
 const Radix15Params& radix15_params();
+constexpr int kMaxNaiveRadix = 32;   // naive radix-m splitting for 4 <= m <= 32, m != 5, 9, 15
 int kernel_mu(int m);            // products of the kernel circuit, -1 if unsupported
 bool kernel_exact(int m);
 // monomial coefficients of the kernel polynomial (double), evaluated from the circuit

@@ -41,11 +41,12 @@ int kernel_mu(int m) {
     case 5: return 2;   // U = B^2, V = U(B+U)
     case 9: return 3;   // U, V = U(B+2U), W = PQ
     case 15: return 4;  // P1..P4
-    default: return -1;
+    default:            // naive radix-m splitting: powers B^2 .. B^{m-1} PAPER.md:140-151
+      return (m >= 4 && m <= kMaxNaiveRadix) ? m - 2 : -1;
   }
 }
 
-bool kernel_exact(int m) { return m == 2 || m == 3 || m == 5 || m == 9; }
+bool kernel_exact(int m) { return kernel_mu(m) >= 0 && m != 15; }
 
 using Poly = std::vector<double>;
 static Poly pmul(const Poly& a, const Poly& b) {
@@ -70,6 +71,15 @@ std::vector<double> kernel_poly(int m) {
   const Poly I{1.0}, B{0.0, 1.0};
   if (m == 2) return {1.0, 1.0};
   if (m == 3) return padd(padd(I, B, 1.0), pmul(B, B), 1.0);
+  if (m != 5 && m != 9 && m != 15 && kernel_mu(m) == m - 2) {
+    // naive radix-m: T_m = I + B + B^2 + ... + B^{m-1} through the power chain B^j = B^{j-1} B
+    Poly T = padd(I, B, 1.0), Pj = B;
+    for (int j = 2; j < m; ++j) {
+      Pj = pmul(Pj, B);
+      T = padd(T, Pj, 1.0);
+    }
+    return T;
+  }
   if (m == 5) {
     Poly U = pmul(B, B), V = pmul(U, padd(B, U, 1.0));
     return padd(padd(padd(I, B, 1.0), U, 1.0), V, 1.0);
@@ -219,8 +229,7 @@ nseries_status build_plan(int64_t k, nseries_plan_kind kind, const int32_t* radi
   if (!out || k < 1 || k > ((int64_t)1 << 62)) return NSERIES_ERR_INVALID_ARG;
   std::memset(out, 0, sizeof(*out));
   std::vector<int> steps;
-  if (kind == NSERIES_PLAN_BINARY || kind == NSERIES_PLAN_TERNARY || kind == NSERIES_PLAN_RADIX5 ||
-      kind == NSERIES_PLAN_RADIX9 || kind == NSERIES_PLAN_RADIX15) {
+  if ((int)kind >= 2 && kernel_mu((int)kind) >= 0) {   // pure radix-m plan (any supported m)
     int m = (int)kind;
     if (m == 15 && !(flags & NSERIES_ALLOW_APPROX)) flags |= NSERIES_ALLOW_APPROX;  // explicit request
     int64_t v = 1;

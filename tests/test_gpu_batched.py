@@ -107,30 +107,23 @@ def test_batched_empty_and_too_big(h):
 @pytest.mark.parametrize("rows", [128, 256])
 def test_config4(h, steps, rows):
     # BASELINE.json configs[3]: 16384 MIMO matrices 32x32 fp32 (rows=256: convergent variant, R12).
-    # the full oracle (V = I) on a seeded sample of 1024 matrices, plus every one
-    # of the 16384 matrices on 2 seeded probe columns (oracle C-1 on fl32(A_b), 2e-5)
+    # SURVEY 8(d) T6 asks for the full oracle on a 1024-matrix sample; the batched C-1 oracle is
+    # fast enough to take EVERY matrix in full (V = I, fl32(A_b), relative Frobenius <= 2e-5)
     Ab = inputs.cfg4(rows=rows)
     S = _batch(h, Ab, steps, torch.float32)
     assert np.all(np.isfinite(S))
     k = OP.plan_reaches(steps)
     n, d = Ab.shape[0], Ab.shape[1]
-    rng = np.random.default_rng(99)
-    sample = np.sort(rng.choice(n, 1024, replace=False))
-    eye = np.broadcast_to(np.eye(d), (len(sample), d, d))
-    ref = O.series_sum_batch(Ab[sample], k, eye)
-    errs = [O.rel_fro(S[b], ref[i]) for i, b in enumerate(sample)]
-    assert max(errs) <= TOL32, max(errs)
-    # all 16384: 2 seeded probe columns per matrix (1 unit + 1 Gaussian), S_gpu V in long double
-    prng = np.random.default_rng(1000 + 3)
-    Vb = np.zeros((n, d, 2))
-    Vb[np.arange(n), prng.integers(0, d, n), 0] = 1.0
-    Vb[:, :, 1] = prng.standard_normal((n, d))
-    ref = O.series_sum_batch(Ab, k, Vb)
-    got = np.einsum("bij,bjp->bip", S.astype(np.float64).astype(np.longdouble), Vb.astype(np.longdouble))
-    num = np.sqrt(np.sum((got - ref) ** 2, axis=(1, 2)))
-    den = np.sqrt(np.sum(ref ** 2, axis=(1, 2)))
-    worst = float(np.max(num / den))
-    assert worst <= TOL32, worst
+    worst, worst_b = 0.0, -1
+    for b0 in range(0, n, 2048):
+        blk = slice(b0, min(n, b0 + 2048))
+        ref = O.series_sum_batch(Ab[blk], k, np.broadcast_to(np.eye(d), (blk.stop - b0, d, d)))
+        got = S[blk].astype(np.float64).astype(np.longdouble)
+        e = np.sqrt(np.sum((got - ref) ** 2, axis=(1, 2))) / np.sqrt(np.sum(ref ** 2, axis=(1, 2)))
+        if float(e.max()) > worst:
+            worst, worst_b = float(e.max()), b0 + int(e.argmax())
+    print(f"config 4 {steps} rows={rows}: worst relative Frobenius over {n} matrices {worst:.3e} (matrix {worst_b})")
+    assert worst <= TOL32, (worst, worst_b)
 
 
 @pytest.mark.parametrize("d,pad", [(32, 0), (32, 1), (31, 3), (8, 0)])
@@ -154,3 +147,18 @@ def test_batched_many_per_warp_strided(h, d, pad):
     S = S[:, : d * d].reshape(batch, d, d)
     for b in list(range(0, batch, 397)) + [batch - 1]:
         assert O.rel_fro(S[b], _oracle(Ab[b].astype(np.float64), [9, 9])) <= TOL32, b
+
+
+@pytest.mark.parametrize("d,dtype", [(32, torch.float32), (17, torch.float32), (48, torch.float32), (32, torch.float64)])
+@pytest.mark.parametrize("steps", [[7, 7], [11, 9], [13], [1, 4, 4]])
+def test_batched_naive_radix(h, d, dtype, steps):
+    # naive radix-m splitting through the one-launch batched kernels
+    rng = np.random.default_rng(40 + d)
+    batch = 5
+    Ab = 0.6 * rng.standard_normal((batch, d, d)) / np.sqrt(d)
+    if dtype == torch.float32:
+        Ab = Ab.astype(np.float32)
+    S = _batch(h, Ab, steps, dtype)
+    tol = TOL32 if dtype == torch.float32 else TOL64
+    for b in range(batch):
+        assert O.rel_fro(S[b], _oracle(Ab[b].astype(np.float64), steps)) <= tol, (d, steps, b)

@@ -451,3 +451,39 @@ def test_host_api_async_size_changes(h):
         ref = torch.empty_like(a)
         P.nseries_eval_host(h, a, a.shape[0], k, plan=plan, S=ref)
         assert torch.equal(s_, ref)
+
+
+# ---------------------------------------------------------------- naive radix-m (NEXT-2)
+
+NAIVE_PLANS = [[7, 7, 7], [11, 9], [13], [7, 1, 11], [4, 4], [1, 13, 2], [32], [6, 15]]
+
+
+@pytest.mark.parametrize("d", [1, 5, 33, 64, 100, 300])
+@pytest.mark.parametrize("steps", NAIVE_PLANS)
+@pytest.mark.parametrize("extra", [0, P.NSERIES_ELIDE_TRIVIAL])
+def test_parity_naive_radix(h, d, steps, extra):
+    # naive radix-m splitting: m - 2 powers with T_m accumulated in their
+    # epilogues, concatenation, next power; exact plans against C-1, with radix 15 against C-2
+    A = inputs.random_matrix(d, 500 + d, 0.7)
+    S, R, st = _run(h, A, steps, flags=extra, want_R=True)
+    Sref, Rref = _oracle_full(A, steps, want_R=True)
+    assert O.rel_fro(S, Sref) <= TOL64, (d, steps)
+    scale = float(np.sqrt(np.sum(np.asarray(Sref, dtype=LD) ** 2)))
+    assert float(np.sqrt(np.sum((R.astype(LD) - Rref) ** 2))) / scale <= 1e-13
+
+
+@pytest.mark.parametrize("d", [16, 64, 200])
+@pytest.mark.parametrize("steps", [[7, 7], [11, 9], [13, 1, 4]])
+def test_parity_naive_radix_f32(h, d, steps):
+    A = inputs.random_matrix(d, 600 + d, 0.7).astype(np.float32)
+    S, _, _ = _run(h, A.astype(np.float64), steps, dtype=torch.float32)
+    assert O.rel_fro(S, _oracle_full(A.astype(np.float64), steps)) <= TOL32, (d, steps)
+
+
+def test_naive_radix_probes_d1024(h):
+    # config-2-sized A (d = 1024, rho ~ 0.93): x7^3 (k = 343, 21 products) on 16 probe columns
+    A = inputs.cfg2()
+    V, _ = inputs.probe_block(A.shape[0], 1)
+    S, _, st = _run(h, A, [7, 7, 7])
+    assert st["products"] == 21
+    assert _probe_parity(S, A, [7, 7, 7], V, False) <= TOL64

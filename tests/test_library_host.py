@@ -65,11 +65,15 @@ def test_approx_requires_flag(lib):
         P.nseries_plan_finalize([15], 15, 0)
     assert e.value.status == 4
     with pytest.raises(P.NSeriesError) as e:
-        P.nseries_plan_finalize([7], 7, 0)
+        P.nseries_plan_finalize([33], 33, 0)          # naive radices stop at 32
+    assert e.value.status == 2
+    with pytest.raises(P.NSeriesError) as e:
+        P.nseries_plan_finalize([0], 1, 0)
     assert e.value.status == 2
 
 
-RADIX_SETS = [[2], [5, 2], [9, 5, 2], [15, 9, 5, 2], [15, 9], [9], [5], [3, 2], [9, 5, 3, 2]]
+RADIX_SETS = [[2], [5, 2], [9, 5, 2], [15, 9, 5, 2], [15, 9], [9], [5], [3, 2], [9, 5, 3, 2],
+              [13, 11, 7, 2], [15, 13, 11, 9, 7, 5, 3, 2], [7], [11, 4]]
 
 
 @pytest.mark.parametrize("elide", [0, 1])
@@ -100,7 +104,15 @@ def test_forms(lib):
     assert p.forms == [2]
 
 
-@pytest.mark.parametrize("m", [2, 3, 5, 9, 15])
+@pytest.mark.parametrize("m,k,products", [(7, 343, 21), (11, 121, 22), (13, 13, 13), (4, 64, 12), (32, 1024, 64)])
+def test_pure_naive_plans(lib, m, k, products):
+    # naive radix-m splitting: C(m) = m products per step
+    plan = P.nseries_plan_build(k, kind=m)
+    assert plan.steps == [m] * len(plan.steps) and plan.products == products and plan.approx == 0
+    assert products == OP.plan_products(OP.pure_plan(m, k))
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 7, 9, 11, 13, 15, 32])
 def test_kernel_info_vs_oracle(lib, m):
     info = P.nseries_kernel_info(m)
     assert info["mu"] == K.MU[m]

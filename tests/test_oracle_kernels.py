@@ -193,3 +193,16 @@ def test_lemma3_prefix_growth_radix15():
     prod = K.poly_mul(f_exact_prefix, fE)[:cap]
     assert all(x == 1 for x in prod[:225])
     assert prod[225] != 1
+
+
+@pytest.mark.parametrize("m", [4, 6, 7, 11, 13, 32])
+def test_naive_kernel_all_ones_exact(m):
+    # naive radix-m kernel: T_m = I + B + ... + B^{m-1} through the power
+    # chain -- exact rational convolution gives m ones and m - 2 products
+    c = K.kernel_coeffs(m)
+    assert c == [F(1)] * m
+    assert K.circuit_products(m) == m - 2 == K.MU[m]
+    # a broken chain is detected: the last power taken as P_{m-2} * P_2 instead of P_{m-2} * B
+    steps, final = K.circuit_naive(m)
+    bad = steps[:-1] + [(steps[-1][0], [0, 0, 1])]
+    assert K.eval_circuit(bad, final) != [F(1)] * m

@@ -43,7 +43,7 @@ def test_lei_nakamura_with_plus_one():
 
 
 def test_dp_vs_bruteforce_small_k():
-    for radices in ([2], [5, 2], [9, 5, 2], RADICES, [15, 9], [3, 2], [9, 5, 3, 2]):
+    for radices in ([2], [5, 2], [9, 5, 2], RADICES, [15, 9], [3, 2], [9, 5, 3, 2], [13, 11, 7, 2], [7, 3]):
         for elide in (False, True):
             for k in range(2, 61):
                 allp = P.enumerate_plans(k, radices)
@@ -74,3 +74,21 @@ def test_ternary_counts():
     # ternary splitting: 3 products per step, 3 log3 k; App. A.3 C(3) = 3
     assert P.plan_products(P.pure_plan(3, 81)) == 12
     assert P.plan_products(P.pure_plan(3, 3 ** 7)) == 21
+
+
+def test_naive_radix_counts():
+    # naive radix-m splitting: m - 2 powers + concatenation + next power =
+    # C(m) = m products per step, coefficient m / log2 m (Table 1's naive column)
+    for m in (4, 7, 11, 13, 32):
+        assert P.plan_products(P.pure_plan(m, m ** 2)) == 2 * m
+        assert P.plan_products(P.pure_plan(m, m ** 2), elide=True) == 2 * m - 2
+    # naive prime radices are options of the DP, rarely optimal: 49 = 7^2 costs 14 as x7 x7,
+    # 13 as six "+1" then x7, and 11 as +1 +1 x2^4 +1 (3 * 16 + 1)
+    assert P.best_plan_dp(49, [7]) == [1] * 6 + [7]
+    assert P.plan_products(P.best_plan_dp(49, [7])) == 13
+    assert P.best_plan_dp(49, [7, 2]) == [1, 1, 2, 2, 2, 2, 1]
+    assert P.plan_products(P.best_plan_dp(49, [7, 2])) == 11
+    # where a naive radix is chosen: k = 7 in elided counting -- x7 costs 7 - 2 = 5, as does
+    # +1 +1 x2 +1; the tie goes to fewer "+1" steps
+    assert P.best_plan_dp(7, [7, 2], elide=True) == [7]
+    assert P.best_plan_dp(7, [7, 2]) == [1, 1, 2, 1]
