@@ -152,6 +152,11 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
     for (int j = 0; j < C::kNI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int KT = (d + BK - 1) / BK;
+  // programmatic dependent launch: everything above overlaps the tail of the previous GEMM of
+  // the plan; its outputs (this GEMM's operands and aux values) are read only after the wait.
+  // This CTA lets the next GEMM be scheduled right away (it waits for our completion itself).
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) load_stage(s, s);
@@ -318,6 +323,25 @@ __global__ void identity_f64_kernel(double* I, int d) {
     I[idx] = (idx / d == idx % d) ? 1.0 : 0.0;
 }
 
+// Launch with the programmatic-stream-serialization attribute (PDL): the kernel may start while
+// the previous kernel on the stream drains; it synchronises with griddepcontrol.wait before
+// touching that kernel's outputs.  NSERIES_PDL=0 launches without it (A/B harness).
+template <typename Kern, typename... Args>
+int launch_pdl(Kern kern, int grid, int threads, size_t smem, cudaStream_t s, Args... args) {
+  static const bool pdl = !(std::getenv("NSERIES_PDL") && std::atoi(std::getenv("NSERIES_PDL")) == 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return (int)cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2, bool SYM>
 int launch_cfg_t(const double* X, const double* Y, int d, const EpiParams& ep, cudaStream_t s) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
@@ -327,8 +351,7 @@ int launch_cfg_t(const double* X, const double* Y, int d, const EpiParams& ep, c
   static_assert(!SYM || BM == BN, "symmetric mode assumes square tiles");
   const int M = ep.rows > 0 ? ep.rows : d;
   const int tiles = SYM ? nt * (nt + 1) / 2 : ((M + BM - 1) / BM) * ((d + BN - 1) / BN);
-  kern<<<tiles, C::kThreads, C::kSmem, s>>>(X, Y, d, ep);
-  return (int)cudaGetLastError();
+  return launch_pdl(kern, tiles, C::kThreads, C::kSmem, s, X, Y, d, ep);
 }
 
 // the symmetric variant is a separate instantiation: the general kernel is unchanged by it
