@@ -54,7 +54,9 @@ typedef enum {
   NSERIES_ERR_OOM = 6,              /* workspace allocation failed                   */
   NSERIES_ERR_CUDA = 7,             /* CUDA runtime / launch error (sticky)          */
   NSERIES_ERR_NO_DEVICE = 8,        /* no sm_100 device                              */
-  NSERIES_ERR_UNSUPPORTED_SIZE = 9  /* e.g. batched path with d > 64                 */
+  NSERIES_ERR_UNSUPPORTED_SIZE = 9, /* e.g. batched path with d > 64                 */
+  NSERIES_ERR_NONFINITE = 10        /* NSERIES_CHECK_FINITE: S has NaN / Inf entries (the
+                                       result is written; not sticky)                  */
 } nseries_status;
 
 typedef enum {
@@ -83,7 +85,10 @@ typedef enum {
 #define NSERIES_RFORM_TELESCOPE  0x4u /* radix-15 residual update as R' = I - f + f R instead
                                          of the paper's R' = I - M Y' (PAPER.md:557 vs 573)   */
 #define NSERIES_NO_GRAPH         0x8u /* do not capture/replay the op list as a CUDA graph     */
-#define NSERIES_SYNC_STATS       0x10u/* record per-op CUDA events for nseries_last_stats      */
+#define NSERIES_SYNC_STATS       0x10u/* time the eval on the device: the op list runs eagerly
+                                         (no graph), an event at every plan-step boundary gives
+                                         stats.ms_step[], the call synchronizes the stream; also
+                                         one NVTX range per plan step                          */
 #define NSERIES_SYMMETRIC        0x20u/* caller asserts A = A^T (fp64, d > 64): every value of
                                          the plan is a polynomial in A, hence symmetric, so each
                                          product computes only the tiles on/above the diagonal and
@@ -94,6 +99,13 @@ typedef enum {
                                          the copy-in of one matrix overlaps the evaluation of the
                                          previous one.  S_host / R_host are valid and A_host may
                                          be reused only after nseries_host_sync.                */
+#define NSERIES_CHECK_FINITE     0x80u/* count NaN / Inf entries of S (fused into the final
+                                         epilogue of the tiled fp64 engine and the batched
+                                         warp kernel, one extra pass over S elsewhere); the
+                                         call synchronizes the stream and returns
+                                         NSERIES_ERR_NONFINITE if the count is nonzero
+                                         (stats.nonfinite).  SURVEY F5: config 4's divergent
+                                         matrices (rho > 1) overflow fp32 for large k.      */
 
 #define NSERIES_MAX_STEPS 128
 
@@ -120,13 +132,23 @@ typedef struct {
 } nseries_plan;
 
 typedef struct {
-  int32_t products;        /* GEMMs launched by the last eval (== plan.products)            */
-  int32_t launches;        /* all kernel launches of the last eval (GEMMs + degenerate ops)  */
+  int32_t products;        /* GEMMs executed by the last eval (== products_exec)            */
+  int32_t launches;        /* kernel launches of the last eval (GEMMs + degenerate ops; 1 for
+                              the single-launch small / batched kernels; + the finite check) */
   int32_t graph_replayed;  /* 1 if the last eval replayed a cached CUDA graph                */
   int32_t n_ops;
   float   ms_total;        /* device time of the last eval (NSERIES_SYNC_STATS only, else 0) */
   int32_t gathers;         /* row-block gathers of the last nseries_eval_sharded (else 0)   */
   int32_t gathers_prefetched; /* of which issued ahead, overlapping the previous product    */
+  int32_t products_paper;  /* the paper's count for the plan (Table 2 counting, PAPER.md:693-709:
+                              mu_m + 2 per radix step incl. S_1 = I and the final power, 1 per
+                              "+1"), whatever the flags                                    */
+  int32_t products_exec;   /* GEMMs actually executed (ELIDE_TRIVIAL: -2; R_out keeps the final
+                              power); a batched eval counts per matrix                      */
+  int32_t n_steps_timed;   /* entries of ms_step[] set (NSERIES_SYNC_STATS with per-op launches;
+                              0 for the single-launch small / batched kernels)              */
+  float   ms_step[NSERIES_MAX_STEPS]; /* device time of each plan step                      */
+  int32_t nonfinite;       /* NSERIES_CHECK_FINITE: NaN / Inf entries of S (else 0)         */
 } nseries_stats;
 
 /* ---- lifecycle ---------------------------------------------------------------------- */

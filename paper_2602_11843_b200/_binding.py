@@ -12,7 +12,7 @@ STATUS_NAMES = {
     0: "NSERIES_OK", 1: "NSERIES_ERR_INVALID_ARG", 2: "NSERIES_ERR_UNSUPPORTED_RADIX",
     3: "NSERIES_ERR_PLAN_K_MISMATCH", 4: "NSERIES_ERR_APPROX_TELESCOPE", 5: "NSERIES_ERR_ALIAS",
     6: "NSERIES_ERR_OOM", 7: "NSERIES_ERR_CUDA", 8: "NSERIES_ERR_NO_DEVICE",
-    9: "NSERIES_ERR_UNSUPPORTED_SIZE",
+    9: "NSERIES_ERR_UNSUPPORTED_SIZE", 10: "NSERIES_ERR_NONFINITE",
 }
 NSERIES_F64, NSERIES_F32 = 0, 1
 NSERIES_PLAN_AUTO, NSERIES_PLAN_BINARY, NSERIES_PLAN_TERNARY, NSERIES_PLAN_RADIX5 = 0, 2, 3, 5
@@ -24,6 +24,7 @@ NSERIES_NO_GRAPH = 0x8
 NSERIES_SYNC_STATS = 0x10
 NSERIES_SYMMETRIC = 0x20
 NSERIES_HOST_ASYNC = 0x40
+NSERIES_CHECK_FINITE = 0x80
 NSERIES_MAX_STEPS = 128
 
 # every symbol include/nseries.h declares (tests check the .so exports exactly these)
@@ -57,7 +58,9 @@ class nseries_stats(ctypes.Structure):
     _fields_ = [("products", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("graph_replayed", ctypes.c_int32), ("n_ops", ctypes.c_int32),
                 ("ms_total", ctypes.c_float), ("gathers", ctypes.c_int32),
-                ("gathers_prefetched", ctypes.c_int32)]
+                ("gathers_prefetched", ctypes.c_int32), ("products_paper", ctypes.c_int32),
+                ("products_exec", ctypes.c_int32), ("n_steps_timed", ctypes.c_int32),
+                ("ms_step", ctypes.c_float * NSERIES_MAX_STEPS), ("nonfinite", ctypes.c_int32)]
 
 
 class nseries_solve_info(ctypes.Structure):
@@ -305,7 +308,9 @@ def nseries_last_stats(h):
     _check(load_library().nseries_last_stats(h, ctypes.byref(s)), "nseries_last_stats")
     return {"products": s.products, "launches": s.launches, "graph_replayed": s.graph_replayed,
             "n_ops": s.n_ops, "ms_total": s.ms_total, "gathers": s.gathers,
-            "gathers_prefetched": s.gathers_prefetched}
+            "gathers_prefetched": s.gathers_prefetched, "products_paper": s.products_paper,
+            "products_exec": s.products_exec, "ms_step": [s.ms_step[i] for i in range(s.n_steps_timed)],
+            "nonfinite": s.nonfinite}
 
 
 __all__ = [n for n in dir() if n.startswith(("nseries_", "NSERIES_"))] + [

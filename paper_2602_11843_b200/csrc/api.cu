@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 using namespace nseries;
@@ -42,7 +44,7 @@ struct nseries_ctx {
   cudaStream_t copy_stream = nullptr;
   // CUDA-graph cache: one executable graph per (program, d, dtype, buffer pointers)
   cudaStream_t cap_stream = nullptr;
-  struct CachedGraph { cudaGraphExec_t exec; int launches; };
+  struct CachedGraph { cudaGraphExec_t exec; int launches; bool nf_fused; };
   std::map<std::string, CachedGraph> graphs;
   // small fp64 single matrices (d <= 64): 0 = one launch of the 4 x 2 cluster kernel when the
   // plan fits (default), 1 = tiled engine (NSERIES_SMALL_MODE, for tests)
@@ -65,6 +67,18 @@ struct nseries_ctx {
   cudaStream_t last_eval_stream = nullptr;
   cudaStream_t gather_stream = nullptr;      // prefetching gathers run here
   cudaEvent_t ev_gready = nullptr, ev_gdone[2] = {nullptr, nullptr};
+  // NSERIES_CHECK_FINITE: device counter of NaN/Inf entries of S and its pinned host copy;
+  // nf_active is set while an eval with the flag enqueues its ops (engines that count in
+  // their final epilogue take it and set nf_fused)
+  int* nf_dev = nullptr;
+  int* nf_host = nullptr;
+  int* nf_active = nullptr;
+  bool nf_fused = false;
+  // NSERIES_SYNC_STATS: one event per plan-step boundary (eager launches)
+  std::vector<cudaEvent_t> ev_step;
+  bool step_timing = false;
+  bool eager = false;   // ops launched directly (not captured): NVTX range per plan step
+  int steps_marked = 0;
 };
 
 namespace {
@@ -121,6 +135,29 @@ nseries_status ensure_splitk(nseries_ctx* h, int d) {
   return NSERIES_OK;
 }
 
+// NSERIES_CHECK_FINITE: zeroed device counter on the stream (allocated once per handle)
+nseries_status begin_check(nseries_ctx* h, cudaStream_t s) {
+  if (!h->nf_dev) {
+    if (cudaMalloc(&h->nf_dev, sizeof(int)) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
+    if (cudaMallocHost(&h->nf_host, sizeof(int)) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
+  }
+  return cuda_fail(h, cudaMemsetAsync(h->nf_dev, 0, sizeof(int), s));
+}
+// read the count back (synchronizes the stream); NONFINITE if any entry was NaN / Inf
+nseries_status finish_check(nseries_ctx* h, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(h->nf_host, h->nf_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  h->stats.nonfinite = *h->nf_host;
+  return *h->nf_host > 0 ? NSERIES_ERR_NONFINITE : NSERIES_OK;
+}
+// the paper's product count of a plan (Table 2 counting, no elision)
+int paper_products(const nseries_plan& p) {
+  int c = 0;
+  for (int i = 0; i < p.n_steps; ++i) c += step_products(p.step[i], i == 0, i + 1 == p.n_steps, 0u);
+  return c;
+}
+
 nseries_status ensure_identity(nseries_ctx* h, int d, nseries_dtype dt, cudaStream_t s) {
   if (h->ident && h->ident_d == d && h->ident_dt == dt) return NSERIES_OK;
   if (h->ident) {
@@ -168,6 +205,28 @@ nseries_status resolve_plan(const nseries_plan* plan, int64_t k, uint32_t flags,
 // Slot i < n_slots holds temp value i's planes; slots n_slots..+2 hold the operand planes of
 // the user's A, S and R buffers (their x planes are the user buffers, ld = d).
 constexpr int kF32Planes = 5;
+// NSERIES_SYNC_STATS: record the event of plan step op.step before the first op of the step,
+// and an NVTX range per plan step (eager launches only: a captured graph replays without host
+// code, so graph evals carry one range around the whole call)
+void mark_step(nseries_ctx* h, const Program& P, int i, int i_end, cudaStream_t s) {
+  (void)i_end;
+  const int st = P.ops[i].step;
+  if (i > 0 && P.ops[i - 1].step == st) return;
+  if (h->step_timing && st >= 0 && st < (int)h->ev_step.size()) {
+    cudaEventRecord(h->ev_step[st], s);
+    ++h->steps_marked;
+  }
+  if (h->eager) {
+    char name[64];
+    std::snprintf(name, sizeof(name), "nseries step %d (%s)", st, P.ops[i].tag);
+    nvtxRangePushA(name);
+  }
+}
+void end_step(nseries_ctx* h, const Program& P, int i, int i_end) {
+  const int st = P.ops[i].step;
+  if (h->eager && (i + 1 == i_end || P.ops[i + 1].step != st)) nvtxRangePop();
+}
+
 // record h->ev_S if op i writes the final S (eval_host overlaps the copy-out of S with the rest)
 void mark_final_S(nseries_ctx* h, const Program& P, int i, cudaStream_t s) {
   if (!h->want_ev_S) return;
@@ -262,6 +321,7 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
       ep.gamma[j] = op.gamma[j];
       for (int a = 0; a < kMaxAux; ++a) ep.beta[j][a] = op.beta[j][a];
     }
+    mark_step(h, P, (int)i, (int)P.ops.size(), s);
     int rc;
     if (op.gemm) {
       const int l = lr[i].first, r = lr[i].second;
@@ -273,6 +333,7 @@ nseries_status run_program_f32(nseries_ctx* h, const Program& P, const float* A,
     }
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
     mark_final_S(h, P, (int)i, s);
+    end_step(h, P, (int)i, (int)P.ops.size());
     ++nl;
   }
   *launches = nl;
@@ -312,12 +373,21 @@ nseries_status run_program_range(nseries_ctx* h, const Program& P, const void* A
       ep.sumsq = sumsq_ptr;
       ep.sumsq_out = sumsq_out;
     }
+    if (h->nf_active && op.gemm)   // NSERIES_CHECK_FINITE counted in the epilogue writing S
+      for (int j = 0; j < op.n_out; ++j)
+        if (op.out[j] == P.final_S) {
+          ep.nonfinite = h->nf_active;
+          ep.nf_out = j;
+          h->nf_fused = true;
+        }
     ep.sym = sym ? 1 : 0;
+    mark_step(h, P, i, i1, s);
     const int rc = op.gemm ? launch_gemm_f64(static_cast<const double*>(ptr(op.X)),
                                              static_cast<const double*>(ptr(op.Y)), d, ep, s)
                            : launch_axpby_f64(d, ep, s);
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
     mark_final_S(h, P, i, s);
+    end_step(h, P, i, i1);
     ++nl;
   }
   *launches = nl;
@@ -607,6 +677,7 @@ const char* nseries_status_string(nseries_status s) {
     case NSERIES_ERR_CUDA: return "CUDA error";
     case NSERIES_ERR_NO_DEVICE: return "no sm_100 device";
     case NSERIES_ERR_UNSUPPORTED_SIZE: return "unsupported size";
+    case NSERIES_ERR_NONFINITE: return "result has NaN / Inf entries";
   }
   return "unknown status";
 }
@@ -658,6 +729,9 @@ nseries_status nseries_destroy(nseries_handle h) {
     if (h->ev_out[b]) cudaEventDestroy(h->ev_out[b]);
   }
   if (h->ev_gready) cudaEventDestroy(h->ev_gready);
+  if (h->nf_dev) cudaFree(h->nf_dev);
+  if (h->nf_host) cudaFreeHost(h->nf_host);
+  for (cudaEvent_t e : h->ev_step) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_gdone)
     if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
@@ -744,7 +818,25 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     if (st != NSERIES_OK) return st;
   }
   const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
-  if (timing) cudaEventRecord(h->ev0, s);
+  const bool check = (flags & NSERIES_CHECK_FINITE) != 0;
+  if (check && (st = begin_check(h, s)) != NSERIES_OK) return st;
+  if (timing) {
+    while ((int)h->ev_step.size() < p.n_steps) {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(h, cudaGetLastError());
+      h->ev_step.push_back(e);
+    }
+    cudaEventRecord(h->ev0, s);
+  }
+  h->nf_active = check ? h->nf_dev : nullptr;
+  h->nf_fused = false;
+  h->step_timing = timing;
+  h->steps_marked = 0;
+  h->eager = timing || (flags & NSERIES_NO_GRAPH);
+  struct Reset {   // per-call executor state, cleared on every return path
+    nseries_ctx* h;
+    ~Reset() { h->nf_active = nullptr; h->step_timing = false; h->eager = false; }
+  } reset{h};
   int launches = 0;
   auto run = [&](cudaStream_t st_) {
     return dt == NSERIES_F64
@@ -754,12 +846,12 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
                                  (flags & NSERIES_SYMMETRIC) != 0);
   };
   bool replayed = false;
-  if (!(flags & NSERIES_NO_GRAPH)) {
+  if (!h->eager) {
     // The op list is replayed as one CUDA graph: the pointers are baked in, so the key holds
     // them; capture runs on a private stream (the caller's may be the legacy NULL stream).
     char ptrs[224];
-    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%p|%d|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
-                  h->sk_ws, (flags & NSERIES_SYMMETRIC) ? 1 : 0, h->want_ev_S ? 1 : 0);
+    std::snprintf(ptrs, sizeof(ptrs), "|%d|%d|%p|%p|%p|%p|%p|%p|%d|%d|%d", d, (int)dt, A, S, R_out, h->ws, h->ident,
+                  h->sk_ws, (flags & NSERIES_SYMMETRIC) ? 1 : 0, h->want_ev_S ? 1 : 0, check ? 1 : 0);
     const std::string gkey = key + ptrs;
     auto git = h->graphs.find(gkey);
     if (git == h->graphs.end()) {
@@ -781,10 +873,11 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
       e = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(h, e);
-      git = h->graphs.emplace(gkey, nseries_ctx::CachedGraph{exec, launches}).first;
+      git = h->graphs.emplace(gkey, nseries_ctx::CachedGraph{exec, launches, h->nf_fused}).first;
     } else {
       replayed = true;
       launches = git->second.launches;
+      h->nf_fused = git->second.nf_fused;
     }
     cudaError_t e = cudaGraphLaunch(git->second.exec, s);
     if (e != cudaSuccess) return cuda_fail(h, e);
@@ -792,8 +885,15 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     st = run(s);
     if (st != NSERIES_OK) return st;
   }
+  if (check && !h->nf_fused) {   // paths without a fused count: one pass over S
+    const int rc = launch_count_nonfinite(dt, S, 0, nullptr, 1, d, d, h->nf_dev, s);
+    if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    ++launches;
+  }
   h->stats = nseries_stats{};
   h->stats.products = P.products;
+  h->stats.products_exec = P.products;
+  h->stats.products_paper = paper_products(p);
   h->stats.launches = launches;
   h->stats.graph_replayed = replayed ? 1 : 0;
   h->stats.n_ops = (int)P.ops.size();
@@ -802,8 +902,17 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     cudaEventRecord(h->ev1, s);
     cudaEventSynchronize(h->ev1);
     cudaEventElapsedTime(&h->stats.ms_total, h->ev0, h->ev1);
+    // per-step times when the ops ran one launch per op (the single-launch d <= 64 kernel
+    // records no step events)
+    if (h->steps_marked == p.n_steps) {
+      h->stats.n_steps_timed = p.n_steps;
+      for (int i = 0; i < p.n_steps; ++i)
+        cudaEventElapsedTime(&h->stats.ms_step[i], h->ev_step[i], i + 1 < p.n_steps ? h->ev_step[i + 1] : h->ev1);
+    }
   }
-  return cuda_fail(h, cudaGetLastError());
+  st = cuda_fail(h, cudaGetLastError());
+  if (st == NSERIES_OK && check) st = finish_check(h, s);
+  return st;
 }
 
 nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d, int64_t k,
@@ -935,22 +1044,28 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
   }
   const Program& P = it->second;
   if ((int)P.ops.size() > kMaxBatchedOps) return NSERIES_ERR_UNSUPPORTED_SIZE;
+  const bool check = (flags & NSERIES_CHECK_FINITE) != 0;
   if (dt == NSERIES_F32 && d <= 32) {
     WarpProgram wp{};
     nseries_status wst = build_warp_program(P, &wp);
     if (wst != NSERIES_OK) return wst;
     h->stats = nseries_stats{};
-    h->stats.products = P.products;
+    h->stats.products = h->stats.products_exec = P.products;
+    h->stats.products_paper = paper_products(p);
     h->stats.n_ops = wp.n_ops;
     if (batch == 0) return NSERIES_OK;
     if ((!A && !A_ptrs) || (!S && !S_ptrs)) return NSERIES_ERR_INVALID_ARG;
     if (A && A == S) return NSERIES_ERR_ALIAS;
     cudaSetDevice(h->device);
-    int rc = launch_batched_warp_f32(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, wp, stream);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (check && (st = begin_check(h, s)) != NSERIES_OK) return st;
+    // NSERIES_CHECK_FINITE counted in the kernel's final epilogue
+    int rc = launch_batched_warp_f32(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, wp, stream,
+                                     check ? h->nf_dev : nullptr);
     if (rc == -1) return NSERIES_ERR_UNSUPPORTED_SIZE;
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
     h->stats.launches = 1;
-    return NSERIES_OK;
+    return check ? finish_check(h, s) : NSERIES_OK;
   }
   BatchedProgram bp{};
   bp.n_ops = (int)P.ops.size();
@@ -989,17 +1104,24 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
     }
   }
   h->stats = nseries_stats{};
-  h->stats.products = P.products;
+  h->stats.products = h->stats.products_exec = P.products;
+  h->stats.products_paper = paper_products(p);
   h->stats.n_ops = bp.n_ops;
   if (batch == 0) return NSERIES_OK;
   if ((!A && !A_ptrs) || (!S && !S_ptrs)) return NSERIES_ERR_INVALID_ARG;
   if (A && A == S) return NSERIES_ERR_ALIAS;
   cudaSetDevice(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (check && (st = begin_check(h, s)) != NSERIES_OK) return st;
   int rc = launch_batched(dt, A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, bp, stream);
   if (rc == -1) return NSERIES_ERR_UNSUPPORTED_SIZE;
   if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
-  h->stats.launches = 1;
-  return NSERIES_OK;
+  if (check) {   // one pass over the batch's S
+    rc = launch_count_nonfinite(dt, S, strideS, S_ptrs, batch, d, d, h->nf_dev, stream);
+    if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+  }
+  h->stats.launches = check ? 2 : 1;
+  return check ? finish_check(h, s) : NSERIES_OK;
 }
 
 nseries_status nseries_eval_batched_strided(nseries_handle h, const void* A, int64_t strideA,
@@ -1106,7 +1228,7 @@ nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t
   inf.prefix = prefix;
   cudaFree(d_ssq);
   h->stats = nseries_stats{};
-  h->stats.products = products;
+  h->stats.products = h->stats.products_exec = h->stats.products_paper = products;
   h->stats.launches = launches;
   h->stats.n_ops = op0;
   if (info) *info = inf;
@@ -1154,7 +1276,7 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
     launches = 3;
   }
   h->stats = nseries_stats{};
-  h->stats.products = 1;
+  h->stats.products = h->stats.products_exec = h->stats.products_paper = 1;
   h->stats.launches = launches;
   h->stats.n_ops = 1;
   return cuda_fail(h, (cudaError_t)rc);
@@ -1260,14 +1382,26 @@ nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shard
   st = ensure_identity(h, d, NSERIES_F64, s);    // I as a full right factor / its row blocks
   if (st != NSERIES_OK) return st;
   const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
+  const bool check = (flags & NSERIES_CHECK_FINITE) != 0;
+  if (check && (st = begin_check(h, s)) != NSERIES_OK) return st;
   if (timing) cudaEventRecord(h->ev0, s);
   int launches = 0, gathers = 0, prefetched = 0;
   st = run_sharded(h, P, reinterpret_cast<const double* const*>(A_shards), reinterpret_cast<double* const*>(S_shards),
                    reinterpret_cast<double* const*>(R_shards), n_local, first_shard, nshards, d, s, &launches,
                    &gathers, &prefetched);
   if (st != NSERIES_OK) return st;
+  if (check) {   // this process's row blocks of S
+    for (int i = 0; i < n_local; ++i) {
+      int r0, rows;
+      shard_range(d, nshards, first_shard + i, &r0, &rows);
+      const int rc = launch_count_nonfinite(NSERIES_F64, S_shards[i], 0, nullptr, 1, rows, d, h->nf_dev, s);
+      if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+      ++launches;
+    }
+  }
   h->stats = nseries_stats{};
-  h->stats.products = P.products;
+  h->stats.products = h->stats.products_exec = P.products;
+  h->stats.products_paper = paper_products(p);
   h->stats.launches = launches;
   h->stats.n_ops = (int)P.ops.size();
   h->stats.gathers = gathers;
@@ -1277,7 +1411,9 @@ nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shard
     cudaEventSynchronize(h->ev1);
     cudaEventElapsedTime(&h->stats.ms_total, h->ev0, h->ev1);
   }
-  return cuda_fail(h, cudaGetLastError());
+  st = cuda_fail(h, cudaGetLastError());
+  if (st == NSERIES_OK && check) st = finish_check(h, s);
+  return st;
 }
 
 }  // extern "C"

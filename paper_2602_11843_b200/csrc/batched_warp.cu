@@ -286,7 +286,9 @@ __device__ __forceinline__ void warp_epilogue(const DevOp& op, float* ws, int d,
 template <int NBW>
 __device__ __forceinline__ void warp_epilogue_final(const DevOp& op, float* ws, float* Sg, int d,
                                                     bool vec_out, int g, int t, int nb0,
-                                                    const float (&big)[2][NBW][4], const float (&sml)[2][NBW][4]) {
+                                                    const float (&big)[2][NBW][4], const float (&sml)[2][NBW][4],
+                                                    int* nonfinite) {
+  int nonfin = 0;   // NSERIES_CHECK_FINITE: NaN/Inf entries of the final S
 #pragma unroll
   for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
@@ -314,6 +316,7 @@ __device__ __forceinline__ void warp_epilogue_final(const DevOp& op, float* ws, 
           if (r == c + 1 && r < d) v1 += op.gamma[o];
           if (op.out[o] != kNoOff) *reinterpret_cast<float2*>(ws + op.out[o] + off) = make_float2(v0, v1);
           if (op.gmask & (1 << o)) {
+            nonfin += ((r < d && c < d && !isfinite(v0)) ? 1 : 0) + ((r < d && c + 1 < d && !isfinite(v1)) ? 1 : 0);
             if (vec_out) {
               *reinterpret_cast<float2*>(Sg + r * 32 + c) = make_float2(v0, v1);
             } else if (r < d) {
@@ -323,12 +326,17 @@ __device__ __forceinline__ void warp_epilogue_final(const DevOp& op, float* ws, 
           }
         }
       }
+  if (nonfinite) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nonfin += __shfl_xor_sync(0xffffffffu, nonfin, o);
+    if (((threadIdx.x & 31) == 0) && nonfin) atomicAdd(nonfinite, nonfin);
+  }
 }
 
 // One fused op for the group's matrix (this warp's column tiles).
 template <int WPM>
 __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, int d, bool vec_out, int g, int t,
-                                        int nb0, int group) {
+                                        int nb0, int group, int* nonfinite) {
   constexpr int NBW = 4 / WPM;
   float big[2][NBW][4], sml[2][NBW][4];
   const int kind = op.kind;
@@ -357,7 +365,7 @@ __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, i
   }
 #endif
   if (op.gmask) {
-    warp_epilogue_final<NBW>(op, ws, Sg, d, vec_out, g, t, nb0, big, sml);
+    warp_epilogue_final<NBW>(op, ws, Sg, d, vec_out, g, t, nb0, big, sml, nonfinite);
   } else switch (op.epi) {
 #define NSERIES_EPI(NA, NO) \
   case NA * 4 + NO: warp_epilogue<NBW, NA, NO>(op, ws, d, g, t, nb0, big, sml); break;
@@ -377,7 +385,7 @@ template <int WPM>
 __global__ void __launch_bounds__(256 * WPM, 1)
 batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const float* const* __restrict__ A_ptrs,
                         float* __restrict__ S, int64_t strideS, float* const* __restrict__ S_ptrs, int batch,
-                        int d, const __grid_constant__ WarpProgram prog) {
+                        int d, const __grid_constant__ WarpProgram prog, int* __restrict__ nonfinite) {
   extern __shared__ __align__(16) float smem_f[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int group = warp / WPM, wig = warp % WPM, groups = (blockDim.x >> 5) / WPM;
@@ -438,7 +446,7 @@ batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const floa
     float* Sg = S_ptrs ? S_ptrs[b] : S + (int64_t)b * strideS;
     const bool vec_out = d == 32 && ((uintptr_t)Sg & 7) == 0;
     const DevOp* ops = sops + cur * prog.n_ops;
-    for (int o = 0; o < prog.n_ops; ++o) warp_op<WPM>(ops[o], ws, Sg, d, vec_out, g, t, nb0, group);
+    for (int o = 0; o < prog.n_ops; ++o) warp_op<WPM>(ops[o], ws, Sg, d, vec_out, g, t, nb0, group, nonfinite);
     cur ^= 1;
   }
   cp_async_wait<0>();
@@ -446,7 +454,8 @@ batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const floa
 
 template <int WPM>
 int launch_wpm(const void* A, int64_t strideA, const void* const* A_ptrs, void* S, int64_t strideS,
-               void* const* S_ptrs, int batch, int d, const WarpProgram& prog, cudaStream_t stream) {
+               void* const* S_ptrs, int batch, int d, const WarpProgram& prog, cudaStream_t stream,
+               int* nonfinite) {
   const size_t per_group = (size_t)(prog.n_slots + 2) * kSlotF * sizeof(float);
   const size_t prog_bytes = 2 * (size_t)prog.n_ops * sizeof(DevOp);
   const int groups = (int)std::min<size_t>(8, (227 * 1024 - prog_bytes) / per_group);
@@ -464,7 +473,7 @@ int launch_wpm(const void* A, int64_t strideA, const void* const* A_ptrs, void* 
   const int grid = std::max(1, std::min((batch + groups - 1) / groups, sms * per_sm));
   kern<<<grid, groups * WPM * 32, smem, stream>>>(
       static_cast<const float*>(A), strideA, reinterpret_cast<const float* const*>(A_ptrs),
-      static_cast<float*>(S), strideS, reinterpret_cast<float* const*>(S_ptrs), batch, d, prog);
+      static_cast<float*>(S), strideS, reinterpret_cast<float* const*>(S_ptrs), batch, d, prog, nonfinite);
   return (int)cudaGetLastError();
 }
 
@@ -522,14 +531,14 @@ nseries_status build_warp_program(const Program& P, WarpProgram* out, bool inpla
 
 int launch_batched_warp_f32(const void* A, int64_t strideA, const void* const* A_ptrs, void* S,
                             int64_t strideS, void* const* S_ptrs, int batch, int d,
-                            const WarpProgram& prog, void* stream) {
+                            const WarpProgram& prog, void* stream, int* nonfinite) {
   if (d > 32) return -1;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const char* env = getenv("NSERIES_BATCHED_WPM");   // tuning knob (1, 2 or 4 warps per matrix)
   const int wpm = env ? atoi(env) : 2;
-  if (wpm == 1) return launch_wpm<1>(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, prog, s);
-  if (wpm == 4) return launch_wpm<4>(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, prog, s);
-  return launch_wpm<2>(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, prog, s);
+  if (wpm == 1) return launch_wpm<1>(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, prog, s, nonfinite);
+  if (wpm == 4) return launch_wpm<4>(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, prog, s, nonfinite);
+  return launch_wpm<2>(A, strideA, A_ptrs, S, strideS, S_ptrs, batch, d, prog, s, nonfinite);
 }
 
 }  // namespace nseries

@@ -210,6 +210,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
   // ---- fused epilogue: out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I
   const int n_aux = ep.n_aux, n_out = ep.n_out;
   double ssq = 0.0;   // optional fused residual norm (sum of squares of out[sumsq_out])
+  int nonfin = 0;     // optional NaN/Inf count of out[nf_out] (NSERIES_CHECK_FINITE)
 #pragma unroll
   for (int i = 0; i < C::kMI; ++i) {
     const int row = m0 + wm0 + i * 8 + g;
@@ -247,6 +248,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
           if (grow == col) v0 += ep.gamma[o];
           if (grow == col + 1) v1 += ep.gamma[o];
           double* const od = static_cast<double*>(ep.out[o]);
+          if (o == ep.nf_out) nonfin += (isfinite(v0) ? 0 : 1) + (isfinite(v1) ? 0 : 1);
           if (!diag_tile) {
             if (o == ep.sumsq_out) ssq += (mirror ? 2.0 : 1.0) * (v0 * v0 + v1 * v1);
             *reinterpret_cast<double2*>(od + off) = make_double2(v0, v1);
@@ -283,6 +285,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
             for (int x = 0; x < kMaxAux; ++x)
               if (x < n_aux) v += ep.beta[o][x] * av[x];
             if (grow == col + e) v += ep.gamma[o];
+            if (o == ep.nf_out) nonfin += isfinite(v) ? 0 : 1;
             if (diag_tile && row > col + e) continue;   // written by its mirror element
             const bool twice = mirror || (diag_tile && row < col + e);
             if (o == ep.sumsq_out) ssq += (twice ? 2.0 : 1.0) * v * v;
@@ -297,6 +300,13 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #pragma unroll
     for (int off2 = 16; off2 > 0; off2 >>= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, off2);
     if ((threadIdx.x & 31) == 0 && ssq != 0.0) atomicAdd(ep.sumsq, ssq);
+  }
+  if (ep.nonfinite) {
+    // symmetric diagonal tiles count both mirror positions' values once each (a value computed
+    // for row > col is discarded but equals its mirror), so the count is of computed values
+#pragma unroll
+    for (int off2 = 16; off2 > 0; off2 >>= 1) nonfin += __shfl_xor_sync(0xffffffffu, nonfin, off2);
+    if ((threadIdx.x & 31) == 0 && nonfin) atomicAdd(ep.nonfinite, nonfin);
   }
 }
 

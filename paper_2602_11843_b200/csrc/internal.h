@@ -109,7 +109,12 @@ struct EpiParams {
                                  // and each off-diagonal output tile is also stored transposed
   int rows = 0;                  // row-sharded chain: X, aux and outputs are `rows` x d row blocks
   int row0 = 0;                  // (0: rows = d) starting at global row row0 (I's diagonal offset)
+  int* nonfinite = nullptr;      // NSERIES_CHECK_FINITE: count NaN/Inf entries of out[nf_out]
+  int nf_out = -1;
 };
+// NSERIES_CHECK_FINITE on paths without a fused count: NaN/Inf entries of a (batch of) rows x d S
+int launch_count_nonfinite(nseries_dtype dt, const void* S, int64_t stride, const void* const* S_ptrs, int batch,
+                           int rows, int d, int* count, void* stream);
 
 // Batched small-matrix path: the compiled op list with values mapped to shared-memory slots.
 constexpr int kMaxBatchedOps = 48;
@@ -159,7 +164,7 @@ struct WarpProgram {
 nseries_status build_warp_program(const Program& P, WarpProgram* wp, bool inplace = true);
 int launch_batched_warp_f32(const void* A, int64_t strideA, const void* const* A_ptrs, void* S,
                             int64_t strideS, void* const* S_ptrs, int batch, int d,
-                            const WarpProgram& prog, void* stream);
+                            const WarpProgram& prog, void* stream, int* nonfinite = nullptr);
 
 // fp32 engine (gemm_tf32.cu): operands as tf32 hi/lo planes with leading dimension ldp
 // (multiple of 32): X role row-major (hi, lo), Y role transposed (hiT, loT); epilogue planes:

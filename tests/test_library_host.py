@@ -161,3 +161,29 @@ def test_eval_sharded_rejects_without_device(lib):
     arr = (ctypes.c_void_p * 1)(None)
     st = lib.nseries_eval_sharded(None, arr, 1, 0, 1, 8, 4, None, 0, arr, None, 0, None)
     assert st == 1
+
+
+def test_binding_struct_layouts_match_header(tmp_path):
+    # the ctypes structs mirror include/nseries.h: sizes and field offsets from a C compile
+    import ctypes
+    import subprocess
+    src = tmp_path / "layout.c"
+    fields = {"nseries_stats": [f for f, _ in P.nseries_stats._fields_],
+              "nseries_plan": [f for f, _ in P.nseries_plan._fields_],
+              "nseries_solve_info": [f for f, _ in P._binding.nseries_solve_info._fields_]}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "nseries.h"', "int main(void) {"]
+    for st, fs in fields.items():
+        lines.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f in fs:
+            lines.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    lines.append("return 0; }")
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = dict(l.split() for l in subprocess.check_output([str(exe)], text=True).splitlines())
+    classes = {"nseries_stats": P.nseries_stats, "nseries_plan": P.nseries_plan,
+               "nseries_solve_info": P._binding.nseries_solve_info}
+    for st, cls in classes.items():
+        assert int(out[st]) == ctypes.sizeof(cls), st
+        for f in fields[st]:
+            assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
