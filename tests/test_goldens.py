@@ -86,6 +86,7 @@ def test_cfg3_golden_closed_form(cfg3_factors, name):
     err = O.rel_fro(np.asarray(sv, dtype=np.float64), ref)
     # Q is orthogonal only to ~1e-13 at d = 4096 and the series amplifies it by up to
     # 1/(1 - 0.995)^2; a wrong term, sign or index would show as O(1e-3) or more
+    print(f"{name}: golden vs closed form {err:.2e}")
     assert err <= 1e-8, (name, err)
 
 
@@ -98,4 +99,5 @@ def test_cfg3_f32_golden_near_f64(plan):
     assert m32["A_sha256"] == m64["A_sha256"]             # same A, fl32 applied by the script
     e = O.rel_fro(s32, s64)
     # input rounding alone moves S_k by ~2e-7 at config 3; the two must differ
+    print(f"{plan}: fp32 golden vs fp64 golden {e:.2e}")
     assert 1e-9 < e <= 2e-6, e
