@@ -281,6 +281,7 @@ def run_native(args):
     configs = None
     if world == 1 and not args.no_configs:
         configs = other_configs(P, h, stream)
+    batch_slices = batched_slice_leg(P, h, stream, rank, world, args)
 
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     # (NSERIES_HOST_ASYNC: the calls are pipelined -- matrix i+1's copy-in overlaps evaluation
@@ -333,6 +334,7 @@ def run_native(args):
         "clocks": clocks,
         "per_plan": per_plan,
         "configs": configs,
+        "cfg4_batch_slices": batch_slices,
     }
     P.nseries_destroy(h)
     if rank == 0:
@@ -454,6 +456,43 @@ def other_configs(P, h, stream):
     return out
 
 
+def batched_slice_leg(P, h, stream, rank, world, args):
+    """Config 4 across the ranks: the 16384 matrices split into contiguous
+    batch slices, one per rank, each evaluated by one nseries_eval_batched_strided launch; no
+    collective on the data path (barrier + max-over-ranks timing only).  Strong scaling: the
+    batch is fixed, value = 16384 matrices / the slowest rank's time per batch."""
+    import torch
+    from paper_2602_11843_b200 import inputs
+    Ab = inputs.cfg4()                                   # same seeded batch on every rank
+    n, d = Ab.shape[0], Ab.shape[1]
+    b0, b1 = R.batch_slice(n, world, rank)
+    A = torch.from_numpy(Ab[b0:b1]).cuda()
+    S = torch.empty_like(A)
+    plan = P.nseries_plan_finalize([9, 9], 81, 0)
+    m = b1 - b0
+    run = lambda: P.nseries_eval_batched_strided(h, A, d * d, m, d, 81, plan=plan, S=S, stream=stream)
+    for _ in range(max(args.warmup, 3)):
+        run()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    n_it = max(10, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n_it):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / n_it, world)
+    counts = R.gather_counts(m, world, device="cuda" if world > 1 else "cpu")
+    return {"metric": "matrices/s", "value": n / (ms * 1e-3), "unit": "matrices/s", "n_gpus": world,
+            "scaling": "strong", "ms_per_batch": ms, "plan": "x9^2 k=81 fp32", "batch": n,
+            "matrices_per_rank": counts, "collectives_on_data_path": 0,
+            "hbm_gbs_aggregate": 2 * n * d * d * 4 / (ms * 1e-3) / 1e9,
+            "note": "contiguous batch slices per rank (replicas.batch_slice), one launch per rank per batch"}
+
+
 def _traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_gemm_f64_traffic.json")
@@ -469,6 +508,13 @@ def run_sharded(args):
     """One A (config 5) split into N row blocks, one per rank, gathers over NCCL (NEXT-3)."""
     import torch
     import torch.distributed as dist
+    # NCCL's own per-rank INIT lines (rank, channels, ring / NVLS / P2P transport choice) are
+    # printed to stderr: file descriptor 1 points at stderr until the one JSON line is printed
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
     rank, world, local = dist_setup(args.gpus)
     import paper_2602_11843_b200 as P
     from paper_2602_11843_b200 import inputs
@@ -503,6 +549,9 @@ def run_sharded(args):
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / n
     st = P.nseries_last_stats(h)
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
+    os.close(saved_stdout)
     if rank == 0:
         tf = plan.products * 2.0 * d ** 3 / (ms * 1e-3) / 1e12
         print(json.dumps({
@@ -513,7 +562,8 @@ def run_sharded(args):
                                            "d": d, "k": k, "plan": list(plan.step[:plan.n_steps]),
                                            "products": plan.products, "parallelism": f"row-shard{world}"},
             "tflops": tf, "frac_of_fp64_peak_per_gpu": tf / world / FP64_PEAK_TFLOPS,
-            "gathers": st["gathers"], "gathers_prefetched": st["gathers_prefetched"]}))
+            "gathers": st["gathers"], "gathers_prefetched": st["gathers_prefetched"],
+            "nccl_log": "stderr (NCCL_DEBUG=INFO, SUBSYS=INIT)"}))
     P.nseries_destroy(h)
     return 0
 

@@ -66,7 +66,7 @@ struct nseries_ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_evaldone[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   cudaStream_t last_eval_stream = nullptr;
   cudaStream_t gather_stream = nullptr;      // prefetching gathers run here
-  cudaEvent_t ev_gready = nullptr, ev_gdone[2] = {nullptr, nullptr};
+  cudaEvent_t ev_gready = nullptr, ev_gdone[3] = {nullptr, nullptr, nullptr};
   // NSERIES_CHECK_FINITE: device counter of NaN/Inf entries of S and its pinned host copy;
   // nf_active is set while an eval with the flag enqueues its ops (engines that count in
   // their final epilogue take it and set nf_fused)
@@ -505,28 +505,49 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
     }
   };
   int ng = 0, nl = 0, npf = 0;
-  auto gather = [&](int v, double* dst, cudaStream_t gs) -> nseries_status {
+  // Every gather -- on the critical path or prefetched -- runs on ONE stream (h->gather_stream),
+  // so the NCCL collectives of the communicator are issued and executed in the same order on
+  // every rank (program order of the op list): no two NCCL calls on one communicator are ever
+  // in flight on different streams.  Ordering with the compute stream s is by events only:
+  // the gather stream waits for everything issued on s so far (the producer of the value and
+  // every earlier reader of the destination buffer), s waits for the gather's completion event
+  // before the first reader.
+  if (!h->gather_stream && cudaStreamCreateWithFlags(&h->gather_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cuda_fail(h, cudaGetLastError());
+  if (!h->ev_gready) {
+    cudaError_t e = cudaEventCreateWithFlags(&h->ev_gready, cudaEventDisableTiming);
+    for (int b = 0; b < 3 && e == cudaSuccess; ++b) e = cudaEventCreateWithFlags(&h->ev_gdone[b], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+  }
+  cudaStream_t const gs = h->gather_stream;
+  // gather value v into dst on the gather stream; completion recorded on ev_gdone[b]
+  auto gather = [&](int v, double* dst, int b) -> nseries_status {
     ++ng;
+    cudaError_t e = cudaEventRecord(h->ev_gready, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, h->ev_gready, 0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
     if (!remote) {
       for (int j = 0; j < n_local; ++j) {
         const int g = first + j;
-        cudaError_t e = cudaMemcpyAsync(dst + (size_t)row0[g] * d, blk(v, j), (size_t)rows[g] * d * sizeof(double),
-                                        cudaMemcpyDeviceToDevice, gs);
+        e = cudaMemcpyAsync(dst + (size_t)row0[g] * d, blk(v, j), (size_t)rows[g] * d * sizeof(double),
+                            cudaMemcpyDeviceToDevice, gs);
         if (e != cudaSuccess) return cuda_fail(h, e);
       }
-      return NSERIES_OK;
+    } else {
+      // allgather-v: every shard broadcast from its owner into its rows of the full buffer
+      const NcclApi& nc = nccl();
+      ncclResult_t r = nc.group_start();
+      for (int g = 0; g < nshards && r == ncclSuccess; ++g) {
+        const int owner = g / n_local;
+        double* rows_dst = dst + (size_t)row0[g] * d;
+        const void* src = owner == h->rank ? blk(v, g - first) : rows_dst;
+        r = nc.broadcast(src, rows_dst, (size_t)rows[g] * d, ncclFloat64, owner, h->comm, gs);
+      }
+      const ncclResult_t r2 = nc.group_end();
+      nseries_status st = nccl_fail(h, r != ncclSuccess ? r : r2);
+      if (st != NSERIES_OK) return st;
     }
-    // allgather-v: every shard broadcast from its owner into its rows of the full buffer
-    const NcclApi& nc = nccl();
-    ncclResult_t r = nc.group_start();
-    for (int g = 0; g < nshards && r == ncclSuccess; ++g) {
-      const int owner = g / n_local;
-      double* rows_dst = dst + (size_t)row0[g] * d;
-      const void* src = owner == h->rank ? blk(v, g - first) : rows_dst;
-      r = nc.broadcast(src, rows_dst, (size_t)rows[g] * d, ncclFloat64, owner, h->comm, gs);
-    }
-    const ncclResult_t r2 = nc.group_end();
-    return nccl_fail(h, r != ncclSuccess ? r : r2);
+    return cuda_fail(h, cudaEventRecord(h->ev_gdone[b], gs));
   };
   // producer op of every value (-1: A, I or never produced)
   std::vector<int> producer(P.n_values, -1);
@@ -538,12 +559,7 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
   // stream has not yet waited for.
   bool a_full = false;
   int cached[2] = {-1, -1}, lru = 0;          // lru: the buffer to overwrite next
-  bool pending[2] = {false, false};
-  if (!h->ev_gready) {
-    cudaError_t e = cudaEventCreateWithFlags(&h->ev_gready, cudaEventDisableTiming);
-    for (int b = 0; b < 2 && e == cudaSuccess; ++b) e = cudaEventCreateWithFlags(&h->ev_gdone[b], cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_fail(h, e);
-  }
+  bool pending[3] = {false, false, false};    // gathers into G[0], G[1], A_full not yet awaited on s
   auto cost = [&](int v) {
     const int kd = P.val_kind[v];
     if (kd == V_IDENT) return 0;
@@ -566,12 +582,13 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
     if (kd == V_IDENT) { *out = ident; return NSERIES_OK; }
     if (kd == V_USER_A) {
       if (!a_full) {
-        nseries_status st = gather(v, A_full, s);
+        nseries_status st = gather(v, A_full, 2);
         if (st != NSERIES_OK) return st;
+        pending[2] = true;
         a_full = true;
       }
       *out = A_full;
-      return NSERIES_OK;
+      return wait_pending(2);
     }
     for (int b = 0; b < 2; ++b)
       if (cached[b] == v) {
@@ -580,14 +597,15 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
         *out = G[b];
         return st;
       }
-    const int b = lru;                          // stream order protects earlier readers
+    const int b = lru;                          // earlier readers: ordered by the gather's event wait
     nseries_status st = wait_pending(b);
-    if (st == NSERIES_OK) st = gather(v, G[b], s);
+    if (st == NSERIES_OK) st = gather(v, G[b], b);
     if (st != NSERIES_OK) return st;
+    pending[b] = true;
     cached[b] = v;
     lru = 1 - b;
     *out = G[b];
-    return NSERIES_OK;
+    return wait_pending(b);                     // on the critical path: s waits right away
   };
   for (size_t i = 0; i < P.ops.size(); ++i) {
     const Op& op = P.ops[i];
@@ -608,19 +626,13 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
       const int r2 = right_of(nx);
       const int b2 = cur_buf == 0 ? 1 : 0;
       if (cost(r2) && P.val_kind[r2] != V_USER_A && producer[r2] < (int)i) {
-        if (!h->gather_stream && cudaStreamCreateWithFlags(&h->gather_stream, cudaStreamNonBlocking) != cudaSuccess)
-          return cuda_fail(h, cudaGetLastError());
-        nseries_status st = wait_pending(b2);   // (no-op: only one gather is ever in flight)
+        // buffer b2's previous gather (if any) must have been consumed by s first: its event is
+        // awaited, then the new gather waits for everything s has issued (incl. b2's readers)
+        nseries_status st = wait_pending(b2);
         if (st != NSERIES_OK) return st;
-        // everything issued so far on the main stream (incl. reads of buffer b2) precedes it
-        cudaError_t e = cudaEventRecord(h->ev_gready, s);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(h->gather_stream, h->ev_gready, 0);
-        if (e != cudaSuccess) return cuda_fail(h, e);
-        st = gather(r2, G[b2], h->gather_stream);
+        st = gather(r2, G[b2], b2);
         if (st != NSERIES_OK) return st;
         ++npf;
-        e = cudaEventRecord(h->ev_gdone[b2], h->gather_stream);
-        if (e != cudaSuccess) return cuda_fail(h, e);
         cached[b2] = r2;
         pending[b2] = true;
         lru = 1 - b2;
@@ -645,7 +657,7 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
       ++nl;
     }
   }
-  for (int b = 0; b < 2; ++b) {                 // the caller's stream owns everything at exit
+  for (int b = 0; b < 3; ++b) {                 // the caller's stream owns everything at exit
     nseries_status st = wait_pending(b);
     if (st != NSERIES_OK) return st;
   }

@@ -2,7 +2,8 @@
 
 The single-matrix S_k(A) path is a serial chain of d x d products and does not shard
 ("replicas only"): N ranks each evaluate their own replica and no data-path
-collective exists.  torch.distributed is used only for the barrier around the timed region
+collective exists.  The batched path (config 4) shards by contiguous batch slices
+(batch_slice), again without a collective.  torch.distributed is used only for the barrier around the timed region
 and for the max-over-ranks reduction of the elapsed time; the whole-job value is
 (ranks x steps) / max elapsed.  The same helpers run on CPU with the gloo backend (tests).
 """
@@ -51,6 +52,29 @@ def max_over_ranks(x, world, device=None):
 def aggregate_rate(units_per_rank, elapsed_ms_max, world):
     """Whole-job throughput: all ranks' units / the slowest rank's elapsed time."""
     return world * units_per_rank / (elapsed_ms_max / 1e3)
+
+
+def batch_slice(n, world, rank):
+    """Contiguous slice [b0, b1) of a batch of n independent matrices for `rank` of `world`
+    (the batched path shards by batch slices, no collective): floor(n / world)
+    matrices each, one more for the first n mod world ranks."""
+    if world < 1 or not 0 <= rank < world or n < 0:
+        raise ValueError("bad slice request")
+    q, r = divmod(n, world)
+    b0 = rank * q + min(rank, r)
+    return b0, b0 + q + (1 if rank < r else 0)
+
+
+def gather_counts(local, world, device="cpu"):
+    """All ranks' integers (e.g. matrices each rank evaluated) -- bookkeeping check only."""
+    if world <= 1:
+        return [int(local)]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([int(local)], dtype=torch.int64, device=device)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [int(x.item()) for x in out]
 
 
 def teardown(world):
