@@ -28,6 +28,7 @@ struct nseries_ctx {
   size_t ws_bytes = 0;
   // identity matrix (paper counting multiplies by S_1 = I)
   void* ident = nullptr;
+  size_t ident_bytes = 0;
   int ident_d = 0;
   nseries_dtype ident_dt = NSERIES_F64;
   // host-API staging
@@ -78,6 +79,11 @@ struct nseries_ctx {
   std::vector<cudaEvent_t> ev_step;
   bool step_timing = false;
   bool eager = false;   // ops launched directly (not captured): NVTX range per plan step
+  // stream-ordered buffer lifetime: recorded after every enqueued evaluation (grow_buffer)
+  cudaEvent_t ev_use = nullptr;
+  bool use_recorded = false;
+  void* ssq = nullptr;   // nseries_solve's per-step residual-norm accumulators
+  size_t ssq_bytes = 0;
   int steps_marked = 0;
 };
 
@@ -92,21 +98,35 @@ nseries_status cuda_fail(nseries_ctx* h, cudaError_t e) {
 
 size_t elem_size(nseries_dtype dt) { return dt == NSERIES_F64 ? sizeof(double) : sizeof(float); }
 
-nseries_status ensure_ws(nseries_ctx* h, size_t bytes) {
-  if (bytes <= h->ws_bytes) return NSERIES_OK;
-  if (h->ws) {
-    cudaDeviceSynchronize();
-    cudaFree(h->ws);
-    h->ws = nullptr;
-    h->ws_bytes = 0;
+// Handle buffers (workspace, split-K area, identity, gather buffers, staging) are allocated and
+// retired in stream order (cudaMallocAsync / cudaFreeAsync on the calling stream): a growing
+// buffer's old allocation is freed after the last work that used it -- the stream waits for
+// h->ev_use, recorded after every enqueued evaluation -- with no device-wide synchronisation.
+void mark_use(nseries_ctx* h, cudaStream_t s) {
+  if (!h->ev_use && cudaEventCreateWithFlags(&h->ev_use, cudaEventDisableTiming) != cudaSuccess) return;
+  cudaEventRecord(h->ev_use, s);
+  h->use_recorded = true;
+}
+nseries_status grow_buffer(nseries_ctx* h, void** buf, size_t* cur, size_t bytes, cudaStream_t s) {
+  if (bytes <= *cur) return NSERIES_OK;
+  if (*buf) {
+    cudaError_t e = h->use_recorded ? cudaStreamWaitEvent(s, h->ev_use, 0) : cudaSuccess;
+    if (e == cudaSuccess) e = cudaFreeAsync(*buf, s);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    *buf = nullptr;
+    *cur = 0;
   }
-  cudaError_t e = cudaMalloc(&h->ws, bytes);
-  if (e != cudaSuccess) {
+  if (cudaMallocAsync(buf, bytes, s) != cudaSuccess) {
     cudaGetLastError();
+    *buf = nullptr;
     return NSERIES_ERR_OOM;
   }
-  h->ws_bytes = bytes;
+  *cur = bytes;
   return NSERIES_OK;
+}
+
+nseries_status ensure_ws(nseries_ctx* h, size_t bytes, cudaStream_t s) {
+  return grow_buffer(h, &h->ws, &h->ws_bytes, bytes, s);
 }
 
 // split-K workspace of the fp32 engine at size d (counters zeroed; the kernel re-zeroes them)
@@ -117,22 +137,12 @@ int tf32_small_maxd() {
   return v;
 }
 
-nseries_status ensure_splitk(nseries_ctx* h, int d) {
+nseries_status ensure_splitk(nseries_ctx* h, int d, cudaStream_t s) {
   const size_t bytes = std::max(tf32_splitk_ws_bytes(d), tf32_splitk_ws_bytes_b128(d));
   if (bytes == 0 || bytes <= h->sk_bytes) return NSERIES_OK;
-  if (h->sk_ws) {
-    cudaDeviceSynchronize();
-    cudaFree(h->sk_ws);
-    h->sk_ws = nullptr;
-    h->sk_bytes = 0;
-  }
-  if (cudaMalloc(&h->sk_ws, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return NSERIES_ERR_OOM;
-  }
-  if (cudaMemset(h->sk_ws, 0, bytes) != cudaSuccess) return cuda_fail(h, cudaGetLastError());
-  h->sk_bytes = bytes;
-  return NSERIES_OK;
+  nseries_status st = grow_buffer(h, &h->sk_ws, &h->sk_bytes, bytes, s);
+  if (st != NSERIES_OK) return st;
+  return cuda_fail(h, cudaMemsetAsync(h->sk_ws, 0, bytes, s));   // counters start at zero
 }
 
 // NSERIES_CHECK_FINITE: zeroed device counter on the stream (allocated once per handle)
@@ -160,18 +170,11 @@ int paper_products(const nseries_plan& p) {
 
 nseries_status ensure_identity(nseries_ctx* h, int d, nseries_dtype dt, cudaStream_t s) {
   if (h->ident && h->ident_d == d && h->ident_dt == dt) return NSERIES_OK;
-  if (h->ident) {
-    cudaStreamSynchronize(s);
-    cudaFree(h->ident);
-    h->ident = nullptr;
-  }
   const size_t bytes = dt == NSERIES_F64 ? (size_t)d * d * sizeof(double)
                                           : 2 * (size_t)d * padded_ld(d) * sizeof(float);
-  cudaError_t e = cudaMalloc(&h->ident, bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return NSERIES_ERR_OOM;
-  }
+  h->ident_bytes = 0;                              // contents change: always re-allocate / rewrite
+  nseries_status gst = grow_buffer(h, &h->ident, &h->ident_bytes, bytes, s);
+  if (gst != NSERIES_OK) return gst;
   h->ident_d = d;
   h->ident_dt = dt;
   int rc;
@@ -742,6 +745,8 @@ nseries_status nseries_destroy(nseries_handle h) {
   }
   if (h->ev_gready) cudaEventDestroy(h->ev_gready);
   if (h->nf_dev) cudaFree(h->nf_dev);
+  if (h->ssq) cudaFree(h->ssq);
+  if (h->ev_use) cudaEventDestroy(h->ev_use);
   if (h->nf_host) cudaFreeHost(h->nf_host);
   for (cudaEvent_t e : h->ev_step) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_gdone)
@@ -820,8 +825,8 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
   const Program& P = it->second;
   cudaSetDevice(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = ensure_ws(h, dt == NSERIES_F64 ? (size_t)P.n_slots * d * d * sizeof(double) : f32_ws_bytes(P, d));
-  if (st == NSERIES_OK && dt == NSERIES_F32) st = ensure_splitk(h, d);
+  st = ensure_ws(h, dt == NSERIES_F64 ? (size_t)P.n_slots * d * d * sizeof(double) : f32_ws_bytes(P, d), s);
+  if (st == NSERIES_OK && dt == NSERIES_F32) st = ensure_splitk(h, d, s);
   if (st != NSERIES_OK) return st;
   // the 4 x 2 cluster kernel (fp64, d <= 64) synthesises I in its fragments: no identity buffer
   const bool one_launch = dt == NSERIES_F64 && h->small_mode == 0 && cluster2d_fits(P, d);
@@ -897,6 +902,7 @@ nseries_status nseries_eval(nseries_handle h, const void* A, int32_t d, int64_t 
     st = run(s);
     if (st != NSERIES_OK) return st;
   }
+  mark_use(h, s);
   if (check && !h->nf_fused) {   // paths without a fused count: one pass over S
     const int rc = launch_count_nonfinite(dt, S, 0, nullptr, 1, d, d, h->nf_dev, s);
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
@@ -991,11 +997,8 @@ nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d
     if (e == cudaSuccess) e = cudaEventRecord(h->ev_out[b], h->copy_stream);
     return cuda_fail(h, e);
   }
-  if (need > h->stage_bytes) {
-    if (h->stage) { cudaDeviceSynchronize(); cudaFree(h->stage); h->stage = nullptr; h->stage_bytes = 0; }
-    if (cudaMalloc(&h->stage, need) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
-    h->stage_bytes = need;
-  }
+  nseries_status st = grow_buffer(h, &h->stage, &h->stage_bytes, need, static_cast<cudaStream_t>(stream));
+  if (st != NSERIES_OK) return st;
   char* dA = static_cast<char*>(h->stage);
   char* dS = dA + bytes;
   char* dR = R_host ? dS + bytes : nullptr;
@@ -1007,7 +1010,7 @@ nseries_status nseries_eval_host(nseries_handle h, const void* A_host, int32_t d
   if (!h->copy_stream && cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
     return cuda_fail(h, cudaGetLastError());
   h->want_ev_S = true;
-  nseries_status st = nseries_eval(h, dA, d, k, plan, dt, dS, dR, flags & ~NSERIES_SYNC_STATS, stream);
+  st = nseries_eval(h, dA, d, k, plan, dt, dS, dR, flags & ~NSERIES_SYNC_STATS, stream);
   h->want_ev_S = false;
   if (st != NSERIES_OK) return st;
   e = cudaStreamWaitEvent(h->copy_stream, h->ev_S, 0);
@@ -1076,6 +1079,7 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
                                      check ? h->nf_dev : nullptr);
     if (rc == -1) return NSERIES_ERR_UNSUPPORTED_SIZE;
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
+    mark_use(h, s);
     h->stats.launches = 1;
     return check ? finish_check(h, s) : NSERIES_OK;
   }
@@ -1132,6 +1136,7 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
     rc = launch_count_nonfinite(dt, S, strideS, S_ptrs, batch, d, d, h->nf_dev, stream);
     if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
   }
+  mark_use(h, s);
   h->stats.launches = check ? 2 : 1;
   return check ? finish_check(h, s) : NSERIES_OK;
 }
@@ -1178,14 +1183,16 @@ nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t
   if (st != NSERIES_OK) return st;
   cudaSetDevice(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = ensure_ws(h, (size_t)P.n_slots * d * d * sizeof(double));
+  st = ensure_ws(h, (size_t)P.n_slots * d * d * sizeof(double), s);
   if (st != NSERIES_OK) return st;
   if (P.needs_identity) {
     st = ensure_identity(h, d, NSERIES_F64, s);
     if (st != NSERIES_OK) return st;
   }
-  double* d_ssq = nullptr;
-  if (cudaMalloc(&d_ssq, sizeof(double) * NSERIES_MAX_STEPS) != cudaSuccess) { cudaGetLastError(); return NSERIES_ERR_OOM; }
+  // per-step ||R||_F^2 accumulators: one handle buffer, allocated once
+  st = grow_buffer(h, &h->ssq, &h->ssq_bytes, sizeof(double) * NSERIES_MAX_STEPS, s);
+  if (st != NSERIES_OK) return st;
+  double* const d_ssq = static_cast<double*>(h->ssq);
   cudaMemsetAsync(d_ssq, 0, sizeof(double) * NSERIES_MAX_STEPS, s);
   nseries_solve_info inf{};
   inf.radix = m;
@@ -1211,7 +1218,7 @@ nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t
         if (P.ops[i].out[j] == P.step_B[step]) { rop = i; rout = j; }
     int nl = 0;
     st = run_program_range(h, P, A, Y, R_out, d, s, op0, op1, &nl, rop, rout, d_ssq + step);
-    if (st != NSERIES_OK) { cudaFree(d_ssq); return st; }
+    if (st != NSERIES_OK) return st;
     for (int i = op0; i < op1; ++i) products += P.ops[i].gemm ? 1 : 0;
     launches += nl;
     op0 = op1;
@@ -1219,7 +1226,7 @@ nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t
     double ssq = 0.0;
     cudaError_t e = cudaMemcpyAsync(&ssq, d_ssq + step, sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) { cudaFree(d_ssq); return cuda_fail(h, e); }
+    if (e != cudaSuccess) return cuda_fail(h, e);
     const double res = std::sqrt(ssq) / std::sqrt((double)d);
     inf.history[step] = res;
     inf.steps = step + 1;
@@ -1238,7 +1245,7 @@ nseries_status nseries_solve(nseries_handle h, const void* A, int32_t d, int32_t
   }
   inf.products = products;
   inf.prefix = prefix;
-  cudaFree(d_ssq);
+  mark_use(h, s);
   h->stats = nseries_stats{};
   h->stats.products = h->stats.products_exec = h->stats.products_paper = products;
   h->stats.launches = launches;
@@ -1266,8 +1273,8 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
   } else {
     const int ldp = padded_ld(d);
     const size_t plane = (size_t)d * ldp;
-    nseries_status st = ensure_ws(h, 4 * plane * sizeof(float));
-    if (st == NSERIES_OK) st = ensure_splitk(h, d);
+    nseries_status st = ensure_ws(h, 4 * plane * sizeof(float), static_cast<cudaStream_t>(stream));
+    if (st == NSERIES_OK) st = ensure_splitk(h, d, static_cast<cudaStream_t>(stream));
     if (st != NSERIES_OK) return st;
     float* w = static_cast<float*>(h->ws);
     rc = launch_split_f32(static_cast<const float*>(X), d, w, w + plane, nullptr, nullptr, ldp, d, false, stream);
@@ -1287,6 +1294,7 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
                : launch_gemm_tf32x3(w, w + plane, w + 2 * plane, w + 3 * plane, d, ldp, e32, stream, h->sk_ws);
     launches = 3;
   }
+  mark_use(h, static_cast<cudaStream_t>(stream));
   h->stats = nseries_stats{};
   h->stats.products = h->stats.products_exec = h->stats.products_paper = 1;
   h->stats.launches = launches;
@@ -1375,22 +1383,10 @@ nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shard
   cudaSetDevice(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t rows_max = (size_t)(d + nshards - 1) / nshards;
-  st = ensure_ws(h, (size_t)n_local * P.n_slots * rows_max * d * sizeof(double));
+  st = ensure_ws(h, (size_t)n_local * P.n_slots * rows_max * d * sizeof(double), s);
   if (st != NSERIES_OK) return st;
-  const size_t full_bytes = 3 * (size_t)d * d * sizeof(double);
-  if (full_bytes > h->full_bytes) {
-    if (h->full) {
-      cudaDeviceSynchronize();
-      cudaFree(h->full);
-      h->full = nullptr;
-      h->full_bytes = 0;
-    }
-    if (cudaMalloc(&h->full, full_bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return NSERIES_ERR_OOM;
-    }
-    h->full_bytes = full_bytes;
-  }
+  st = grow_buffer(h, &h->full, &h->full_bytes, 3 * (size_t)d * d * sizeof(double), s);
+  if (st != NSERIES_OK) return st;
   st = ensure_identity(h, d, NSERIES_F64, s);    // I as a full right factor / its row blocks
   if (st != NSERIES_OK) return st;
   const bool timing = (flags & NSERIES_SYNC_STATS) != 0;
@@ -1402,6 +1398,7 @@ nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shard
                    reinterpret_cast<double* const*>(R_shards), n_local, first_shard, nshards, d, s, &launches,
                    &gathers, &prefetched);
   if (st != NSERIES_OK) return st;
+  mark_use(h, s);
   if (check) {   // this process's row blocks of S
     for (int i = 0; i < n_local; ++i) {
       int r0, rows;
