@@ -351,7 +351,9 @@ __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, i
 #pragma unroll
         for (int e = 0; e < 4; ++e) big[mb][j][e] = sml[mb][j][e] = 0.f;
   }
+  NSERIES_SHAKE_POINT(8 * kind + 1);
   group_sync<WPM>(group);   // every operand read of the group precedes any output write (in-place slots)
+  NSERIES_SHAKE_POINT(8 * kind + 2);
 #if defined(NSERIES_BW_PROBE) && NSERIES_BW_PROBE == 1   // tools/bw_probe.cu: mainloop only
   {
     float sum = 0.f;
@@ -376,6 +378,7 @@ __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, i
 #undef NSERIES_EPI
     default: break;
   }
+  NSERIES_SHAKE_POINT(8 * kind + 3);
   group_sync<WPM>(group);
 }
 
@@ -436,12 +439,14 @@ batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const floa
   cp_async_commit();
   for (int b = gg; b < batch; b += ng) {
     const int bn = b + ng;
+    NSERIES_SHAKE_POINT(100 + (b & 7));
     if (bn < batch) {
       const float* p = srcp(bn);
       load_matrix_async<WPM>(abuf0 + (cur ^ 1) * kSlotF, p, d, vec_ok(p), glane);
     }
     cp_async_commit();
     cp_async_wait<1>();
+    NSERIES_SHAKE_POINT(110 + (b & 7));
     group_sync<WPM>(group);
     float* Sg = S_ptrs ? S_ptrs[b] : S + (int64_t)b * strideS;
     const bool vec_out = d == 32 && ((uintptr_t)Sg & 7) == 0;

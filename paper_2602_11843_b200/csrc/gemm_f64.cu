@@ -190,6 +190,7 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #pragma unroll
     for (int k = 0; k < KK; ++k) {
       if (k == KK - 1) {
+        NSERIES_SHAKE_POINT(kt);
         cp_async_wait<STAGES - 2>();   // tile kt+1 has landed
         __syncthreads();
       }

@@ -593,6 +593,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     if (lane == 0) {
       for (int kb = 0; kb < KB; ++kb) {
         const int s = kb % STAGES, r = kb / STAGES;
+        NSERIES_SHAKE_POINT(1000 + kb);
         if (r > 0) mbar_wait(&sm.empty[s], (r - 1) & 1);
 #ifdef NSERIES_TF32_NO_TMA
         mbar_arrive(&sm.full[s]);
@@ -650,6 +651,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       for (int c = 0; c < NC; ++c) {
         const int kb = c / CPS, h = c % CPS, s = kb % STAGES, r = kb / STAGES;
         const int b = c % NBUF, u = c / NBUF;     // accumulator b, use count u
+        NSERIES_SHAKE_POINT(3000 + c);
         if (h == 0 && !full_ok) {
 #ifdef NSERIES_TF32_DEBUG
           long long t1 = clock64();
@@ -764,6 +766,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     for (int i = 0; i < EC; ++i) acc[i] = 0.f;
     for (int c = 0; c < NC; ++c) {
       const int b = c % NBUF, u = c / NBUF;
+      NSERIES_SHAKE_POINT(5000 + c);
       mbar_wait(&sm.tmem_full[b], u & 1);
       fence_after();
       const uint32_t t_acc = tmem + lane_off + b * BN + cb;
@@ -797,6 +800,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
 #endif
       fence_before();
+      NSERIES_SHAKE_POINT(7000 + c);
       if (lane == 0) {
         if constexpr (TWO_SM) mbar_arrive_cluster(mapa_rank(saddr(&sm.tmem_empty[b]), 0));   // leader's
         else mbar_arrive(&sm.tmem_empty[b]);
@@ -841,12 +845,14 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       unsigned* cnt = ep.sk_cnt + 2 * tile;
       float4* const pt = reinterpret_cast<float4*>(ep.sk_part + (size_t)tile * (BN * BM)) + (size_t)(cb / 4) * BM + rl;
       float* const st = tiles + (half * BM + rl) * kStageLd;
+      NSERIES_SHAKE_POINT(9000);
       if (warp == 4 && lane == 0) sm.sk_last = atomicAdd(cnt, 1u) == 1u;
       asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kEpiWarps) : "memory");
       if (!sm.sk_last) {
 #pragma unroll
         for (int i = 0; i < EC; i += 4) __stcg(pt + (size_t)(i / 4) * BM, make_float4(st[i], st[i + 1], st[i + 2], st[i + 3]));
         __threadfence();
+        NSERIES_SHAKE_POINT(9001);
         asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kEpiWarps) : "memory");
         if (warp == 4 && lane == 0) atomicAdd(cnt + 1, 1u);
       } else {

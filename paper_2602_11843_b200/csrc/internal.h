@@ -233,6 +233,27 @@ nseries_status build_cluster2d_program(const Program& P, C2Program* out);
 bool cluster2d_fits(const Program& P, int d);
 int launch_plan_cluster2d_f64(int d, const C2Program& prog, const double* A, double* S, double* R, void* stream);
 
+// Race shaking (harness builds only, -DNSERIES_SHAKE=<seed>; tools/race_shake.py): a seeded
+// pseudo-random __nanosleep of up to ~4 us at a quarter of the hand-synchronised protocol points
+// (mbarrier waits, DSMEM pushes, TMA / MMA issue, drains, split-K counters, group barriers).  A
+// missing wait or barrier shows up as a result that differs from the unshaken build.  Delays
+// are per warp (all lanes sleep alike), so warp-synchronous instructions stay converged.
+#ifdef __CUDACC__
+#ifdef NSERIES_SHAKE
+__device__ __forceinline__ void shake_point(unsigned site) {
+  unsigned h = (blockIdx.x + 1u) * 0x9E3779B1u ^ ((threadIdx.x >> 5) + 1u) * 0x85EBCA77u ^
+               (site + 1u) * 0xC2B2AE3Du ^ (unsigned)(NSERIES_SHAKE) * 0x27D4EB2Fu;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep(h >> 20);
+}
+#define NSERIES_SHAKE_POINT(site) shake_point(site)
+#else
+#define NSERIES_SHAKE_POINT(site) ((void)0)
+#endif
+#endif
+
 // fp64: C-side launchers implemented in gemm_f64.cu.  Return cudaError_t as int.
 int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep, void* stream);
 int launch_axpby_f64(int d, const EpiParams& ep, void* stream);

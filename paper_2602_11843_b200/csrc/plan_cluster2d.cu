@@ -200,6 +200,7 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
 #endif
   for (int o = 0; o < n_ops; ++o) {
     const C2Dev& op = sops[o];
+    NSERIES_SHAKE_POINT(64 * o + 0);
     if (op.wait_bar >= 0 && (o == 0 || sops[o - 1].wait_bar != op.wait_bar)) wait_bar(op.wait_bar);
     __syncthreads();
 #ifdef NSERIES_C2_PROFILE
@@ -230,7 +231,9 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
 #ifdef NSERIES_C2_PROFILE
     if (tid == 0 && rank == 0) g_c2_prof[2 + 3 * o] = clock64() + (long long)(acc[0] * 0.0);
 #endif
+    NSERIES_SHAKE_POINT(64 * o + 1);
     if (op.csync) cluster.sync();
+    NSERIES_SHAKE_POINT(64 * o + 2);
     const uint32_t my_bar = bar_off + 8u * (uint32_t)o;
     double2 av[kMaxAux];
 #pragma unroll
@@ -258,6 +261,7 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
       if (op.out_row[q] >= 0) {
         const int off = op.out_row[q] + swz_row(rl, gcol);
         *reinterpret_cast<double2*>(smc + off) = make_double2(v0, v1);
+        NSERIES_SHAKE_POINT(64 * o + 3 + q);
 #pragma unroll
         for (int cc = 0; cc < CB; ++cc)
           if (cc != cb) {
@@ -269,6 +273,7 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
       if (op.out_col[q] >= 0) {
         const int off = op.out_col[q] + swz_col(grow, cl);
         *reinterpret_cast<double2*>(smc + off) = make_double2(v0, v1);
+        NSERIES_SHAKE_POINT(64 * o + 8 + q);
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr)
           if (rr != rb) {
@@ -292,6 +297,7 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
   // no CTA leaves while pushes into it are in flight: every byte addressed to this CTA has
   // landed once all its mbarriers completed, and nothing else touches a peer's shared memory
   // (st.async carries register values), so no closing cluster barrier is needed
+  NSERIES_SHAKE_POINT(64 * n_ops + 63);
   for (int o = 0; o < n_ops; ++o)
     if (sops[o].tx) wait_bar(o);
 #ifdef NSERIES_C2_END_SYNC
