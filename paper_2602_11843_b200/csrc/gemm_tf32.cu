@@ -648,6 +648,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       // one chunk later and a blocking wait happens only if a probe failed.
       uint32_t full_ok = mbar_test(&sm.full[0], 0);
       uint32_t tm_ok = 1;                        // chunk 0 uses a fresh buffer
+#ifdef NSERIES_TF32_DEBUG
+      long long dbg_wfull = 0, dbg_wempty = 0;   // local sums: one atomic per CTA at the end
+#endif
       for (int c = 0; c < NC; ++c) {
         const int kb = c / CPS, h = c % CPS, s = kb % STAGES, r = kb / STAGES;
         const int b = c % NBUF, u = c / NBUF;     // accumulator b, use count u
@@ -658,7 +661,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
           mbar_wait(&sm.full[s], r & 1);
 #ifdef NSERIES_TF32_DEBUG
-          if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)(clock64() - t1));
+          dbg_wfull += clock64() - t1;
 #endif
         }
         if (u > 0 && !tm_ok) {
@@ -667,7 +670,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #endif
           mbar_wait(&sm.tmem_empty[b], (u - 1) & 1);
 #ifdef NSERIES_TF32_DEBUG
-          if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)(clock64() - t0));
+          dbg_wempty += clock64() - t0;
 #endif
         }
         fence_after();
@@ -739,6 +742,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       if (g_dbg && lane == 0) {
         atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 2, 1ull);
         atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 3, (unsigned long long)(clock64() - tstart));
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)dbg_wempty);
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)dbg_wfull);
       }
 #endif
     }

@@ -1,10 +1,11 @@
 // Harness-only: per-CTA phase breakdown of the fp32 engine at d=4096 (mainloop+drain vs final
 // epilogue) for a 1-output op and a 3-output op shaped like radix-15 G1 (x, hi/lo, hiT/loT + 1 aux).
 #define NSERIES_TF32_DEBUG
+#include <cstdlib>
 #include "../paper_2602_11843_b200/csrc/gemm_tf32.cu"
 using namespace nseries;
 int main() {
-  int d = 4096, ldp = 4096; size_t n = (size_t)d * ldp;
+  int d = getenv("TD") ? atoi(getenv("TD")) : 4096, ldp = d; size_t n = (size_t)d * ldp;
   float *Xh, *Xl, *Yh, *Yl, *C, *P[6];
   cudaMalloc(&Xh, n*4); cudaMalloc(&Xl, n*4); cudaMalloc(&Yh, n*4); cudaMalloc(&Yl, n*4); cudaMalloc(&C, n*4);
   for (int i = 0; i < 6; ++i) { cudaMalloc(&P[i], n * 4); cudaMemset(P[i], 0, n * 4); }
