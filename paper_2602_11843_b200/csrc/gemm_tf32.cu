@@ -67,13 +67,9 @@ namespace {
 #endif
 constexpr int BM = 128, BN = NSERIES_TF32_BN, BK = NSERIES_TF32_BK, STAGES = NSERIES_TF32_STAGES;
 constexpr int CL = NSERIES_TF32_CLUSTER;     // 1 or 2 CTAs per cluster
-#ifndef NSERIES_TF32_2SM
-#define NSERIES_TF32_2SM 0   // (correct, but 1.8x slower: the leader waits for both CTAs' drains every chunk)
-#endif
-// 2-SM UMMA: the CTA pair issues ONE tcgen05.mma.cta_group::2 (M = 256) per k-step from the
-// leader CTA; each CTA holds its 128 A rows and its 128-row half of the B tile (no multicast)
-constexpr bool TWO_SM = NSERIES_TF32_2SM != 0;
-static_assert(!TWO_SM || CL == 2, "2-SM UMMA needs CTA pairs");
+// (A 2-SM UMMA variant -- tcgen05.mma.cta_group::2, M = 256 from the leader CTA -- was correct
+// but 1.8x slower: with the per-16-K drain the leader waits for both CTAs' drains every chunk.
+// Removed in round 2.)
 #ifndef NSERIES_TF32_PREFETCH
 #define NSERIES_TF32_PREFETCH 0   // (8 measured 19% slower at d = 4096: extra L2 traffic)
 #endif
@@ -97,7 +93,6 @@ constexpr int CPS = (BK / 8) / KSC;          // chunks per smem stage
 // Same bias per chunk as KSC = 2 with all three terms, with half the drains per K.
 constexpr bool XACC = NSERIES_TF32_XACC != 0;
 constexpr int NBUF = XACC ? (512 - BN) / BN : 512 / BN;   // TMEM chunk accumulators of BN columns
-static_assert(!XACC || !TWO_SM, "cross accumulator: 1-SM MMAs only");
 #ifndef NSERIES_TF32_EPI_WARPS
 #define NSERIES_TF32_EPI_WARPS 8   // (16: 11% slower -- the single MMA-issue thread competes with 20 warps)
 #endif
@@ -112,14 +107,14 @@ constexpr uint32_t kStageBytes = 2 * kATileBytes + 2 * kBTileBytes;
 constexpr uint32_t kTmemCols = (NBUF + (XACC ? 1 : 0)) * BN <= 256 ? 256 : 512;   // power of two >= used
 constexpr uint32_t kSwizzleLayout = BK == 32 ? 2 : 4;   // UMMA layout: SWIZZLE_128B / _64B
 constexpr uint32_t kAtomBytes = 8 * BK * 4;     // 8 rows x 64 B = 512 B (SBO)
-constexpr int kStageLd = EC + 1;                // epilogue staging row (floats)
+constexpr int kStageLd = EC + 4;                // epilogue staging row (floats, 16-byte aligned)
 
 struct Smem {
   alignas(1024) uint8_t xh[STAGES][kATileBytes];
   alignas(1024) uint8_t xl[STAGES][kATileBytes];
   alignas(1024) uint8_t yh[STAGES][kBTileBytes];
   alignas(1024) uint8_t yl[STAGES][kBTileBytes];
-  uint8_t epi_extra[8192];   // the epilogue staging ((NG+1) x [128][EC+1] fp32) spills past the ring
+  uint8_t epi_extra[8192];   // the epilogue staging ((NG+1) x [128][EC+4] fp32) spills past the ring
   alignas(8) uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tmem_full[NBUF];
@@ -238,36 +233,6 @@ __device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
                    saddr(bar)), "h"(mask)
                : "memory");
 }
-// M = 256 across the CTA pair (leader issues; A rows and B half read from both CTAs' smem)
-constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-__device__ __forceinline__ void mma2_tf32_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
-      " @e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(kIdesc2), "r"(acc));
-}
-__device__ __forceinline__ void mma2_commit_mc_w(uint64_t* bar, uint16_t mask) {
-  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-               " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
-                   saddr(bar)), "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-// TMA whose complete_tx is delivered to the mbarrier at shared::cluster address bar (the leader's)
-__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-          saddr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -352,12 +317,45 @@ __device__ __forceinline__ float rna_tf32_fast(float x) {
 
 #ifdef NSERIES_TF32_DEBUG
 __device__ float* g_dbg = nullptr;
+__device__ unsigned long long* g_tl = nullptr;   // per CTA: globaltimer at start / end, SM id
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #endif
 
 // Fused epilogue of one tile (after both accumulator halves are staged in shared memory).
 // Inlined: an out-of-line version reads the __grid_constant__ parameters through generic loads
 // (~10 K cycles per pass); the drain loop stays spill-free as long as the staging pointer is
 // derived without an integer round trip through the shared-window address.
+//
+// Vectorised (round 2): a lane owns a quad of 4 consecutive columns, so one warp-wide access
+// covers a whole staged row (EC = 128) or two (EC = 64): LDS.128 of the staged accumulator,
+// coalesced LDG.128 of the aux rows and STG.128 of the x / hi / lo planes, with 16-byte aligned
+// staging rows (kStageLd = EC + 4: row-wise and quad-per-row column reads are conflict-free).
+// The transposed planes (and the symmetric mirror) are written by a column pass in which lane =
+// row, reading its row's quad with one LDS.128 and storing 4 coalesced 128-byte columns.
+// Misaligned or ragged quads (d % 4 != 0, tile edges) take a scalar path with the same formulas.
+__device__ __forceinline__ float4 ld4g(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float q4(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+__device__ __forceinline__ float4 rna4(const float4& v) {
+  return make_float4(rna_tf32_fast(v.x), rna_tf32_fast(v.y), rna_tf32_fast(v.z), rna_tf32_fast(v.w));
+}
+__device__ __forceinline__ float4 sub4(const float4& a, const float4& b) {
+  return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+}
+// store the elements of quad t selected by mask (bit e: column c + e) at row pointer p + c
+__device__ __forceinline__ void st_quad(float* p, int c, const float4& t, unsigned mask, bool vec) {
+  if (vec && mask == 0xFu) {
+    *reinterpret_cast<float4*>(p + c) = t;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (mask & (1u << e)) p[c + e] = q4(t, e);
+  }
+}
+
 template <int NO>   // number of outputs (compile-time: the per-element loops fully unroll)
 __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const int m0, const int n0, const int d,
                                            const int ew, const int lane, const EpiParamsF32& ep,
@@ -367,24 +365,44 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* const tiles = reinterpret_cast<float*>(smem_raw + tiles_off);
   float* const vt = tiles + NG * BM * kStageLd;   // output values of the current output
+  constexpr int kQ = EC / 4;                      // column quads per staged row (32 or 16)
+  constexpr int kRPI = 32 / kQ;                   // rows per warp-wide access (1 or 2)
   const int n_aux = ep.n_aux, ldp = ep.ldp;
   constexpr int n_out = NO;
   const float* auxb[kMaxAux];
   int auxld[kMaxAux];
+  // vector path: every aux row and every row-major output row this epilogue touches starts on
+  // a 16-byte boundary (hn0 is a multiple of 4; ldp is a multiple of 32)
+  bool vec = (reinterpret_cast<uintptr_t>(ep.out_hi[0]) | reinterpret_cast<uintptr_t>(ep.out_lo[0])) % 16 == 0;
 #pragma unroll
   for (int x = 0; x < kMaxAux; ++x) {
     auxb[x] = x < n_aux ? ep.aux[x] : nullptr;
     auxld[x] = x < n_aux ? ep.aux_ld[x] : 0;
+    if (x < n_aux) vec = vec && (reinterpret_cast<uintptr_t>(auxb[x]) % 16 == 0) && (auxld[x] % 4 == 0);
   }
+#pragma unroll
+  for (int o = 0; o < kMaxOut; ++o)
+    if (o < n_out)
+      vec = vec && ((reinterpret_cast<uintptr_t>(ep.out_x[o]) | reinterpret_cast<uintptr_t>(ep.out_hi[o]) |
+                     reinterpret_cast<uintptr_t>(ep.out_lo[o])) % 16 == 0) && (ep.out_ld[o] % 4 == 0);
+#ifdef NSERIES_TF32_DEBUG
+  __shared__ long long s_tp[8];
+#define NSERIES_TP(i) do { if (warp == 4 && lane == 0) s_tp[i] = clock64(); } while (0)
+#else
+#define NSERIES_TP(i) do { } while (0)
+#endif
+  NSERIES_TP(0);
+  const int qc = 4 * (lane % kQ);                 // this lane's quad: columns qc .. qc+3 of the half
+  const int rsub = lane / kQ;                     // its row within a warp-wide access
   for (int hh = 0; hh < NG; ++hh) {
     const int hn0 = n0 + hh * EC;            // global column of this column group
     float* const tile = tiles + hh * BM * kStageLd;
     asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
-#ifdef NSERIES_TF32_DEBUG
-    if (warp == 4 && lane == 0 && g_dbg) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 7 + hh, (unsigned long long)(clock64() - t_drained));
-#endif
+    NSERIES_TP(1 + 3 * hh);
     const int ncol = min(EC, d - hn0);       // valid columns of this half (> 0 for launched tiles)
     const int nrow = min(BM, d - m0);
+    // valid columns of this lane's quad
+    const unsigned cmask = qc + 4 <= ncol ? 0xFu : (qc < ncol ? (1u << (ncol - qc)) - 1u : 0u);
     // Pass 0 computes EVERY output from one read of the aux tiles (row-major x / hi / lo planes)
     // and stages the first output that needs transposed planes; each further transposed output
     // gets its own pass (staging only).  fp32 combination (binary64 epilogue arithmetic
@@ -410,105 +428,109 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
         ol[o] = (on && pass == 0) ? ep.out_lo[o] : nullptr;
         old_[o] = o < n_out ? ep.out_ld[o] : 0;
       }
-      // row pass: coalesced aux reads and x / hi / lo writes (lanes along columns).  Rows are
-      // processed in batches of RU whose aux loads are all issued before any use.
+      // row pass: lanes along column quads; batches of RU warp-wide row accesses whose aux
+      // loads are all issued before any use
       constexpr int RU = NSERIES_TF32_RU;
-      for (int rb = ew; rb < BM; rb += kFinalWarps * RU) {
-        float av[RU][EC / 32][kMaxAux];
+      constexpr int kStep = kFinalWarps * kRPI;   // rows advanced per warp per batch element
+      for (int rb = ew * kRPI + rsub; rb < BM; rb += kStep * RU) {
+        float4 av[RU][kMaxAux];
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
-          const int rr = rb + u * kFinalWarps, r = m0 + rr;
-          const bool rok = rr < nrow;
+          const int rr = rb + u * kStep, r = m0 + rr;
+          const bool ok = rr < nrow && cmask != 0u;
 #pragma unroll
           for (int x = 0; x < kMaxAux; ++x) {
-            const float* ar = auxb[x] + (size_t)r * auxld[x] + hn0;
+            av[u][x] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (x < n_aux && ok) {
+              const float* ar = auxb[x] + (size_t)r * auxld[x] + hn0 + qc;
+              if (vec && cmask == 0xFu) {
+                av[u][x] = ld4g(ar);
+              } else {
+                float tmp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int cc = 0; cc < EC / 32; ++cc) {
-              const int cl = cc * 32 + lane;
-              av[u][cc][x] = (x < n_aux && rok && cl < ncol) ? __ldg(ar + cl) : 0.f;
+                for (int e = 0; e < 4; ++e)
+                  if (cmask & (1u << e)) tmp[e] = __ldg(ar + e);
+                av[u][x] = make_float4(tmp[0], tmp[1], tmp[2], tmp[3]);
+              }
             }
           }
         }
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
-          const int rr = rb + u * kFinalWarps, r = m0 + rr;
-          if (rr >= nrow) break;
-          const int dcol = r - hn0;                // tile column holding the diagonal
+          const int rr = rb + u * kStep, r = m0 + rr;
+          if (rr >= nrow || cmask == 0u) continue;
+          const int dq = r - hn0 - qc;             // quad element on the diagonal (if 0..3)
+          // symmetric diagonal tiles: the upper part (column >= row) only
+          unsigned smask = cmask;
+          if (diag_pair) smask &= dq <= 0 ? 0xFu : (dq >= 4 ? 0u : (0xFu << dq) & 0xFu);
+          const float4 a = *reinterpret_cast<const float4*>(tile + rr * kStageLd + qc);
 #pragma unroll
-          for (int cc = 0; cc < EC / 32; ++cc) {
-            const int cl = cc * 32 + lane;
-            if (cl >= ncol) break;
-            const float a = tile[rr * kStageLd + cl];
+          for (int o = 0; o < kMaxOut; ++o) {
+            if (o >= n_out) break;
+            float4 t = make_float4(al[o] * a.x, al[o] * a.y, al[o] * a.z, al[o] * a.w);
 #pragma unroll
-            for (int o = 0; o < kMaxOut; ++o) {
-              if (o >= n_out) break;
-              float t = al[o] * a;
-#pragma unroll
-              for (int x = 0; x < kMaxAux; ++x) t = fmaf(be[o][x], av[u][cc][x], t);   // be = 0 beyond n_aux
-              if (cl == dcol) t += ga[o];
-              if (!diag_pair || cl >= dcol) {   // symmetric diagonal tiles: upper part only
-                if (ox[o]) ox[o][(size_t)r * old_[o] + hn0 + cl] = t;
-                if (oh[o]) {
-                  const float hi = rna_tf32_fast(t);
-                  oh[o][(size_t)r * ldp + hn0 + cl] = hi;
-                  ol[o][(size_t)r * ldp + hn0 + cl] = rna_tf32_fast(t - hi);
-                }
-              }
-              if (o == tout) vt[rr * kStageLd + cl] = t;
+            for (int x = 0; x < kMaxAux; ++x) {   // be = 0 beyond n_aux
+              t.x = fmaf(be[o][x], av[u][x].x, t.x);
+              t.y = fmaf(be[o][x], av[u][x].y, t.y);
+              t.z = fmaf(be[o][x], av[u][x].z, t.z);
+              t.w = fmaf(be[o][x], av[u][x].w, t.w);
             }
+            if (dq == 0) t.x += ga[o];
+            if (dq == 1) t.y += ga[o];
+            if (dq == 2) t.z += ga[o];
+            if (dq == 3) t.w += ga[o];
+            if (ox[o]) st_quad(ox[o] + (size_t)r * old_[o] + hn0, qc, t, smask, vec);
+            if (oh[o]) {
+              const float4 hi = rna4(t);
+              st_quad(oh[o] + (size_t)r * ldp + hn0, qc, hi, smask, vec);
+              st_quad(ol[o] + (size_t)r * ldp + hn0, qc, rna4(sub4(t, hi)), smask, vec);
+            }
+            if (o == tout) *reinterpret_cast<float4*>(vt + rr * kStageLd + qc) = t;
           }
         }
       }
-#ifdef NSERIES_TF32_DEBUG
-      if (warp == 4 && lane == 0 && g_dbg && hh == 0 && pass == 0)
-        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 9, (unsigned long long)(clock64() - t_drained));
-#endif
-      if (tout >= 0 && ep.sym) {
+      if (pass == 0) NSERIES_TP(2 + 3 * hh);
+      if (tout >= 0) {
         asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
-        // symmetric mode: the mirror image (c, r) of every element (r, c) (strictly upper part
-        // in diagonal tiles) into the output's own x / hi / lo planes; lanes along rows
-        float* const mx = ep.out_x[tout];
-        float* const mh = ep.out_hi[tout];
-        float* const ml = ep.out_lo[tout];
-        const int mld = ep.out_ld[tout];
-        for (int cl = ew; cl < ncol; cl += kFinalWarps) {
-          const int c = hn0 + cl;
+        // column pass: lane = row of a 32-row group, one LDS.128 of its row's quad, then four
+        // coalesced 128-byte columns -- of the transposed operand planes, or (symmetric mode)
+        // the mirror image (c, r) of every element (r, c) (strictly upper part in diagonal
+        // tiles) in the output's own x / hi / lo planes
+        float* const tx = ep.sym ? ep.out_x[tout] : nullptr;
+        float* const th = ep.sym ? ep.out_hi[tout] : ep.out_hiT[tout];
+        float* const tl = ep.sym ? ep.out_lo[tout] : ep.out_loT[tout];
+        const int tld = ep.sym ? ep.out_ld[tout] : ldp;   // ld of the x mirror (hi / lo: ldp)
+        for (int item = ew; item < (BM / 32) * kQ; item += kFinalWarps) {
+          const int rr = (item / kQ) * 32 + lane, c0 = 4 * (item % kQ);
+          if (rr >= nrow || c0 >= ncol) continue;
+          const int r = m0 + rr;
+          const float4 v = *reinterpret_cast<const float4*>(vt + rr * kStageLd + c0);
 #pragma unroll
-          for (int rc = 0; rc < BM / 32; ++rc) {
-            const int rr = rc * 32 + lane, r = m0 + rr;
-            if (rr >= nrow) break;
-            if (diag_pair && r >= c) continue;
-            const float v = vt[rr * kStageLd + cl];
-            if (mx) mx[(size_t)c * mld + r] = v;
-            if (mh) {
-              const float hi = rna_tf32_fast(v);
-              mh[(size_t)c * ldp + r] = hi;
-              ml[(size_t)c * ldp + r] = rna_tf32_fast(v - hi);
+          for (int e = 0; e < 4; ++e) {
+            const int c = hn0 + c0 + e;
+            if (c0 + e >= ncol) break;
+            if (ep.sym && diag_pair && r >= c) continue;
+            const float val = q4(v, e);
+            if (tx) tx[(size_t)c * tld + r] = val;
+            if (th) {
+              const float hi = rna_tf32_fast(val);
+              th[(size_t)c * ldp + r] = hi;
+              tl[(size_t)c * ldp + r] = rna_tf32_fast(val - hi);
             }
-          }
-        }
-      } else if (tout >= 0) {
-        asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
-        // column pass: transposed operand planes, lanes along rows of the tile
-        float* const ohT = ep.out_hiT[tout];
-        float* const olT = ep.out_loT[tout];
-        for (int cl = ew; cl < ncol; cl += kFinalWarps) {
-          float* const hr = ohT + (size_t)(hn0 + cl) * ldp + m0;
-          float* const lr = olT + (size_t)(hn0 + cl) * ldp + m0;
-#pragma unroll
-          for (int rc = 0; rc < BM / 32; ++rc) {
-            const int rr = rc * 32 + lane;
-            if (rr >= nrow) break;
-            const float v = vt[rr * kStageLd + cl];
-            const float hi = rna_tf32_fast(v);
-            hr[rr] = hi;
-            lr[rr] = rna_tf32_fast(v - hi);
           }
         }
       }
       asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads));
+      if (pass == 0) NSERIES_TP(3 + 3 * hh);
     }
   }
+#ifdef NSERIES_TF32_DEBUG
+  NSERIES_TP(7);
+  if (warp == 4 && lane == 0 && g_dbg)
+    for (int i = 1; i < 8; ++i)
+      atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 7 + i, (unsigned long long)(s_tp[i] - s_tp[i - 1]));
+#endif
+#undef NSERIES_TP
 }
 
 __global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(CL, 1, 1)
@@ -558,29 +580,29 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   const int NC = KB * CPS;                   // accumulation chunks
 #ifdef NSERIES_TF32_DEBUG
   const long long t_kernel0 = clock64();
+  unsigned long long* const dbgp = reinterpret_cast<unsigned long long*>(g_dbg);   // loaded once
+  if (threadIdx.x == 0 && g_tl) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_tl[3 * blockIdx.x] = gtimer();
+    g_tl[3 * blockIdx.x + 2] = smid;
+  }
   long long t_drained = 0;
 #endif
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], TWO_SM ? 1 : CL); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CL); }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&sm.tmem_full[b], 1);
-      mbar_init(&sm.tmem_empty[b], TWO_SM ? 2 * kEpiWarps : kEpiWarps);   // 2-SM: both CTAs' drains
+      mbar_init(&sm.tmem_empty[b], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
-    if constexpr (TWO_SM) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                       saddr(&sm.tmem_base)),
-                   "r"(kTmemCols));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                       saddr(&sm.tmem_base)),
-                   "r"(kTmemCols));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     saddr(&sm.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   fence_before();
   if (CL > 1) cluster_sync_all();   // the peer's barriers are initialised before any multicast
@@ -598,18 +620,6 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
 #ifdef NSERIES_TF32_NO_TMA
         mbar_arrive(&sm.full[s]);
 #else
-        if constexpr (TWO_SM) {
-          // both CTAs load their A rows and B half to the same offsets of their own smem; the
-          // bytes are accounted on the LEADER's full barrier (2 x own bytes)
-          const int k0 = (kb0 + kb) * BK;
-          const uint32_t fb = mapa_rank(saddr(&sm.full[s]), 0);
-          if (rank == 0) mbar_expect_tx(&sm.full[s], 2 * (2 * kATileBytes + kBTileBytes));
-          tma_load_2d_2sm(sm.xh[s], &mXh, fb, k0, m0);
-          tma_load_2d_2sm(sm.xl[s], &mXl, fb, k0, m0);
-          tma_load_2d_2sm(sm.yh[s], &mYh, fb, k0, n0 + rank * (BN / 2));
-          tma_load_2d_2sm(sm.yl[s], &mYl, fb, k0, n0 + rank * (BN / 2));
-          continue;
-        }
         mbar_expect_tx(&sm.full[s], kStageBytes);
         const int k0 = (kb0 + kb) * BK;
         tma_load_2d(sm.xh[s], &mXh, &sm.full[s], k0, m0);
@@ -634,11 +644,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: the whole warp runs the loop, one elected lane issues
-    // (2-SM UMMA: only the leader CTA issues, for both CTAs of the pair)
-    if (!TWO_SM || rank == 0) {
+    {
 #ifdef NSERIES_TF32_DEBUG
       long long tstart = clock64();
-      if (g_dbg && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 4, (unsigned long long)(tstart - t_kernel0));
+      if (dbgp && lane == 0) atomicAdd(dbgp + 4, (unsigned long long)(tstart - t_kernel0));
 #endif
       // The tensor pipe queues only a couple of MMAs, so a blocking barrier wait between two
       // chunks drains it (tools/tcgen05_rate.cu: 97 clk per N=128 MMA in a producer/consumer
@@ -684,21 +693,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         const uint32_t t_acc = tmem + b * BN;
         // small cross terms first (accumulator still small), hi*hi last; K-major swizzled
         // tiles advance 32 B (8 tf32, +2 in the >>4 address field) per k-step
-        if constexpr (TWO_SM) {
-#pragma unroll
-          for (int j = 0; j < KSC; ++j) {
-            const int ks = h * KSC + j;
-            mma2_tf32_w(t_acc, dxh + 2 * ks, dyl + 2 * ks, j == 0 ? 0u : 1u);
-            mma2_tf32_w(t_acc, dxl + 2 * ks, dyh + 2 * ks, 1u);
-          }
-#pragma unroll
-          for (int j = 0; j < KSC; ++j) {
-            const int ks = h * KSC + j;
-            mma2_tf32_w(t_acc, dxh + 2 * ks, dyh + 2 * ks, 1u);
-          }
-          mma2_commit_mc_w(&sm.tmem_full[b], 3);   // both CTAs' accumulators ready
-          if (h == CPS - 1) mma2_commit_mc_w(&sm.empty[s], 3);
-        } else if constexpr (XACC) {
+        if constexpr (XACC) {
           // hi*hi into this chunk's buffer, then the cross terms into the full-K accumulator
           const uint32_t t_x = tmem + NBUF * BN;
 #pragma unroll
@@ -739,11 +734,11 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
         }
       }
 #ifdef NSERIES_TF32_DEBUG
-      if (g_dbg && lane == 0) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 2, 1ull);
-        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 3, (unsigned long long)(clock64() - tstart));
-        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 0, (unsigned long long)dbg_wempty);
-        atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 1, (unsigned long long)dbg_wfull);
+      if (dbgp && lane == 0) {
+        atomicAdd(dbgp + 2, 1ull);
+        atomicAdd(dbgp + 3, (unsigned long long)(clock64() - tstart));
+        atomicAdd(dbgp + 0, (unsigned long long)dbg_wempty);
+        atomicAdd(dbgp + 1, (unsigned long long)dbg_wfull);
       }
 #endif
     }
@@ -807,8 +802,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
       fence_before();
       NSERIES_SHAKE_POINT(7000 + c);
       if (lane == 0) {
-        if constexpr (TWO_SM) mbar_arrive_cluster(mapa_rank(saddr(&sm.tmem_empty[b]), 0));   // leader's
-        else mbar_arrive(&sm.tmem_empty[b]);
+        mbar_arrive(&sm.tmem_empty[b]);
       }
     }
     if constexpr (XACC) {
@@ -840,7 +834,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     float* const tiles = reinterpret_cast<float*>(smem_raw + (reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw));
     const int rl = q * 32 + lane;
 #pragma unroll
-    for (int i = 0; i < EC; ++i) tiles[(half * BM + rl) * kStageLd + i] = acc[i];
+    for (int i = 0; i < EC; i += 4)   // STS.128: 8-lane phases hit 8 distinct bank quads (pitch EC + 4)
+      *reinterpret_cast<float4*>(tiles + (half * BM + rl) * kStageLd + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
     if (split) {
       // split-K (2 K ranges): the first CTA of the tile to finish leaves its partial, the
       // second adds it (p_0 + p_1 is exact-commutative, so the result does not depend on who
@@ -905,9 +900,9 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     else tile_epilogue<3>(tiles_off, m0, n0, d, ew, lane, ep, warp, td, diag_pair);
   }
 #ifdef NSERIES_TF32_DEBUG
-  if (warp == 4 && lane == 0 && g_dbg) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 5, (unsigned long long)(clock64() - t_drained));
-    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg) + 6, (unsigned long long)(t_drained - t_kernel0));
+  if (warp == 4 && lane == 0 && dbgp) {
+    atomicAdd(dbgp + 5, (unsigned long long)(clock64() - t_drained));
+    atomicAdd(dbgp + 6, (unsigned long long)(t_drained - t_kernel0));
   }
 #endif
   fence_before();
@@ -915,8 +910,10 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
   else __syncthreads();
   if (warp == 2) {
     fence_after();
-    if constexpr (TWO_SM) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
-    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
+#ifdef NSERIES_TF32_DEBUG
+    if (lane == 0 && g_tl) g_tl[3 * blockIdx.x + 1] = gtimer();
+#endif
   }
 }
 
@@ -1050,7 +1047,7 @@ void splitk_plan(int d, bool sym, int* first, int* S) {
   *first = 0;
   *S = 1;
   static const bool off = std::getenv("NSERIES_TF32_SPLITK") && std::atoi(std::getenv("NSERIES_TF32_SPLITK")) == 0;
-  if (sym || off || NSERIES_TF32_2SM) return;
+  if (sym || off) return;
   const int ntn = (d + BN - 1) / BN;
   const int T = ((d + BM - 1) / BM + CL - 1) / CL * ntn;
   const int W = wave_clusters();

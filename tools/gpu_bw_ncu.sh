@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 200 python tools/time_batched.py > gpurun_out/bw_time.txt 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:batched_warp -s 3 -c 1 -o gpurun_out/bw_full -f python tools/time_batched.py > gpurun_out/bw_ncu.log 2>&1
