@@ -36,6 +36,14 @@ FP64_PEAK_SOURCE = "measured: DMMA m8n8k4 register loop, tools/peak_fp64.cu (pro
 # TF32 dense peak: measured bf16 burst (MEASURED_PEAKS.json, 1631.3 TF) x the guide's nominal
 # tf32/bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md) -- "of measured x nominal ratio"
 TF32_PEAK_TFLOPS = 1631.3 * 1.1 / 2.25
+# tcgen05 .kind::tf32 measured on this pool (tools/tcgen05_peak.cu, 4 s sustained, 148 CTAs x
+# M128 N256 K8 from SMEM: 128.0 clk per MMA = the cycle floor; profiles/peaks_r02_tcgen05_tf32.json):
+# 1116 TF/s with all-zero operands (1842 MHz), 916 TF/s with random operands -- the board's power
+# cap holds the SM clock at ~1510 MHz when the tensor cores switch real data.  The random-operand
+# figure is the sustained peak a real 3xTF32 GEMM can reach.
+TCGEN05_TF32_PEAK_TFLOPS = 1116.4
+TCGEN05_TF32_PEAK_RANDOM_TFLOPS = 916.4
+TCGEN05_TF32_FLOP_PER_CLK = 148 * 4096.0   # cycle floor x 148 SMs: 1191 TF/s at 1965 MHz
 # Legacy-path (mma.sync m16n8k8 .tf32) peak used by the batched small-matrix kernel: measured
 # register loop, tools/mma_issue.cu (profiles/peaks_r01_mma_sync.txt)
 MMA_SYNC_TF32_PEAK_TFLOPS = 275.7
@@ -264,6 +272,9 @@ def run_native(args):
                                         "evals_per_s": world * 1e3 / pstep, "tflops": alg,
                                         "tf32_tensor_tflops": 3 * alg,
                                         "tf32_frac_of_peak": 3 * alg / TF32_PEAK_TFLOPS,
+                                        "tf32_frac_of_measured_tcgen05_peak": 3 * alg / TCGEN05_TF32_PEAK_TFLOPS,
+                                        "tf32_frac_of_measured_tcgen05_peak_random_operands":
+                                            3 * alg / TCGEN05_TF32_PEAK_RANDOM_TFLOPS,
                                         "clocks": fclk.summary()}
             with ClockSampler(local) as sclk:
                 sms, _, _ = time_plan(P, h, A32, S32, stp, kk, n, 2, fl | P.NSERIES_SYMMETRIC, stream, world)
@@ -276,6 +287,9 @@ def run_native(args):
             if c.get("sm_mhz") and c.get("sm_max_mhz"):   # power-capped runs: peak at the clock held
                 per_plan[name + " fp32"]["tf32_frac_of_peak_at_held_clock"] = (
                     3 * alg / (TF32_PEAK_TFLOPS * c["sm_mhz"] / c["sm_max_mhz"]))
+                # against the tcgen05 cycle floor at the clock the run held (power cap)
+                per_plan[name + " fp32"]["tf32_frac_of_cycle_floor_at_held_clock"] = (
+                    3 * alg / (TCGEN05_TF32_FLOP_PER_CLK * c["sm_mhz"] * 1e6 / 1e12))
         del A32, S32
 
     configs = None

@@ -15,12 +15,18 @@ __device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t sbo) {
 }
 
 template <int KIND>   // 0: tf32 (K = 8 per MMA), 1: bf16 (K = 16 per MMA)
-__global__ void __launch_bounds__(128, 1) peak(long long iters, unsigned long long* cycles) {
+__global__ void __launch_bounds__(128, 1) peak(long long iters, unsigned long long* cycles, int rnd) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tb;
-  for (int i = threadIdx.x; i < (128 + 256) * 32; i += blockDim.x) reinterpret_cast<float*>(base)[i] = 0.f;
+  // operands: zeros (minimum switching power) or pseudo-random values in (-1, 1) (the power a
+  // real GEMM draws; bf16 reads the same bytes as pairs of random bf16 values)
+  for (int i = threadIdx.x; i < (128 + 256) * 32; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ (blockIdx.x * 40503u + 12345u);
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    reinterpret_cast<float*>(base)[i] = rnd ? ((float)(h >> 8) / 8388608.0f - 1.0f) : 0.f;
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -65,7 +71,7 @@ __global__ void __launch_bounds__(128, 1) peak(long long iters, unsigned long lo
 }
 
 template <int KIND>
-double run(double seconds, int sms, unsigned long long* dcyc, double* clk_per_mma) {
+double run(double seconds, int sms, unsigned long long* dcyc, double* clk_per_mma, int rnd) {
   const size_t smem = 1024 + (128 + 256) * 128;
   cudaFuncSetAttribute(peak<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1;
@@ -75,7 +81,7 @@ double run(double seconds, int sms, unsigned long long* dcyc, double* clk_per_mm
   float ms = 0;
   for (;;) {   // calibrate the loop to the requested time
     cudaEventRecord(e0);
-    peak<KIND><<<sms, 128, smem>>>(iters, dcyc);
+    peak<KIND><<<sms, 128, smem>>>(iters, dcyc, rnd);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
@@ -87,8 +93,9 @@ double run(double seconds, int sms, unsigned long long* dcyc, double* clk_per_mm
   const double kper = KIND == 0 ? 8 : 16;
   const double flops = 2.0 * 128 * 256 * kper * 4 * (double)iters * sms;
   *clk_per_mma = (double)cyc / (4.0 * iters);
-  printf("%s: %.2f s, %.1f TFLOP/s, %.1f cycles per M128 N256 MMA (%s)\n", KIND == 0 ? "tf32 (K=8)" : "bf16 (K=16)",
-         ms / 1e3, flops / (ms * 1e-3) / 1e12, *clk_per_mma, cudaGetErrorString(cudaGetLastError()));
+  printf("%s %s operands: %.2f s, %.1f TFLOP/s, %.1f cycles per M128 N256 MMA, implied SM clock %.0f MHz (%s)\n",
+         KIND == 0 ? "tf32 (K=8)" : "bf16 (K=16)", rnd ? "random" : "zero", ms / 1e3, flops / (ms * 1e-3) / 1e12,
+         *clk_per_mma, (double)cyc / (ms * 1e-3) / 1e6, cudaGetErrorString(cudaGetLastError()));
   return flops / (ms * 1e-3) / 1e12;
 }
 
@@ -98,10 +105,14 @@ int main(int argc, char** argv) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* dcyc;
   cudaMalloc(&dcyc, 8);
-  double c0, c1;
-  const double tf = run<0>(seconds, sms, dcyc, &c0);
-  const double bf = run<1>(seconds, sms, dcyc, &c1);
+  double c0, c1, c2, c3;
+  const double tf = run<0>(seconds, sms, dcyc, &c0, 0);
+  const double bf = run<1>(seconds, sms, dcyc, &c1, 0);
+  const double tfr = run<0>(seconds, sms, dcyc, &c2, 1);
+  const double bfr = run<1>(seconds, sms, dcyc, &c3, 1);
   printf("{\"tf32_tflops\": %.2f, \"tf32_clk_per_mma_n256\": %.1f, \"bf16_tflops\": %.2f, \"bf16_clk_per_mma_n256\": %.1f, "
-         "\"seconds_each\": %.1f, \"sms\": %d}\n", tf, c0, bf, c1, seconds, sms);
+         "\"tf32_tflops_random\": %.2f, \"tf32_clk_per_mma_n256_random\": %.1f, \"bf16_tflops_random\": %.2f, "
+         "\"bf16_clk_per_mma_n256_random\": %.1f, \"seconds_each\": %.1f, \"sms\": %d}\n",
+         tf, c0, bf, c1, tfr, c2, bfr, c3, seconds, sms);
   return 0;
 }
