@@ -187,9 +187,11 @@ plan_cluster2d_f64_kernel(int d, const double* __restrict__ A, double* __restric
   auto wait_bar = [&](int b) {
     const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bars + b));
     uint32_t done = 0;
-    while (!done)
+    for (uint32_t i = 0; !done; ++i) {   // bounded: a protocol bug traps instead of hanging the GPU
       asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
                    : "=r"(done) : "r"(a) : "memory");
+      if (i > (1u << 26)) __trap();
+    }
   };
   cluster.sync();
   const int rl = 8 * mt + g;                 // this lane's block row (epilogue) / A-fragment row

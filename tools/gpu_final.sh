@@ -1,0 +1,12 @@
+#!/bin/bash
+# Harness: full GPU check of the tree -- GPU test suite, bench, ncu launch list of the bench step
+# (run plain first), one --set full capture each of the fp64 and fp32 engines.  Outputs in gpurun_out/.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-per-plan --no-configs"
+$CMD > gpurun_out/plain_short.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_f64 -s 6 -c 1 -o gpurun_out/prof_gemm_f64 -f $CMD > gpurun_out/ncu_full_f64.log 2>&1
+TIME_D=4096 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tf32x3 -s 5 -c 1 -o gpurun_out/prof_tf32 -f python tools/time_f32_gemm.py > gpurun_out/ncu_full_tf32.log 2>&1
+echo done > gpurun_out/final_done.txt
