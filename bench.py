@@ -43,7 +43,6 @@ TF32_PEAK_TFLOPS = 1631.3 * 1.1 / 2.25
 # figure is the sustained peak a real 3xTF32 GEMM can reach.
 TCGEN05_TF32_PEAK_TFLOPS = 1116.4
 TCGEN05_TF32_PEAK_RANDOM_TFLOPS = 916.4
-TCGEN05_TF32_FLOP_PER_CLK = 148 * 4096.0   # cycle floor x 148 SMs: 1191 TF/s at 1965 MHz
 # Legacy-path (mma.sync m16n8k8 .tf32) peak used by the batched small-matrix kernel: measured
 # register loop, tools/mma_issue.cu (profiles/peaks_r01_mma_sync.txt)
 MMA_SYNC_TF32_PEAK_TFLOPS = 275.7
@@ -287,9 +286,7 @@ def run_native(args):
             if c.get("sm_mhz") and c.get("sm_max_mhz"):   # power-capped runs: peak at the clock held
                 per_plan[name + " fp32"]["tf32_frac_of_peak_at_held_clock"] = (
                     3 * alg / (TF32_PEAK_TFLOPS * c["sm_mhz"] / c["sm_max_mhz"]))
-                # against the tcgen05 cycle floor at the clock the run held (power cap)
-                per_plan[name + " fp32"]["tf32_frac_of_cycle_floor_at_held_clock"] = (
-                    3 * alg / (TCGEN05_TF32_FLOP_PER_CLK * c["sm_mhz"] * 1e6 / 1e12))
+
         del A32, S32
 
     configs = None
