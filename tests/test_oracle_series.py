@@ -272,3 +272,50 @@ def test_series_sum_batch(oracle_lib):
     closed = ((1 - a ** k) / (1 - a))[:, None] * Vb[2].astype(LD)
     assert O.rel_fro(out[2], closed) <= 1e-17
     assert O.series_sum_batch(Ab[:0], k, Vb[:0]).shape == (0, d, 3)
+
+
+# ---------------------------------------------------------------- App. "approximate kernels"
+
+# PAPER.md:955-977 (Table tab:approx): single kernel application on d = 64 with A's eigenvalues
+# geometrically spaced in [0.01, 1] (rho(B) = 0.99, B = I - A), error ||S - A^{-1}||_2 /
+# ||A^{-1}||_2; PAPER.md:984-993 prints the radix-33 kernel's polynomial to 2 decimals.
+_R33_PRINTED = [1.00, 1.00, 1.00, 0.98, 1.00, 1.02, 1.00, 0.69, 1.12, 0.99, 1.05,
+                0.88, 1.11, 0.69, 0.73, 1.01, 1.27, 1.04, 1.08, 1.06, 0.98, 1.00,
+                0.99, 0.88, 1.13, 0.95, 1.02, 0.97, 1.01, 0.99, 1.00, 1.00, 1.00]
+
+
+def _approx_table_matrix():
+    lam = np.geomspace(0.01, 1.0, 64)           # eigenvalues of A = I - B
+    return np.diag(1.0 - lam), np.diag(1.0 / lam)
+
+
+def _inv_err(S, Ainv):
+    S = np.asarray(S, dtype=np.float64)
+    return float(np.linalg.norm(S - Ainv, 2) / np.linalg.norm(Ainv, 2))
+
+
+@pytest.mark.parametrize("m,printed", [(7, 0.932), (8, 0.923), (24, 0.786), (27, 0.762)])
+def test_table_approx_exact_rows(oracle_lib, m, printed):
+    # "Standard S_7 / S_8" rows (exact) and the rows whose kernels match the exact radix to the
+    # printed digits ("vs Exact" 1.000): the oracle's S_m gives the printed error
+    B, Ainv = _approx_table_matrix()
+    S, _ = O.series_sum(B, m, np.eye(64))
+    assert round(_inv_err(S, Ainv), 3) == printed
+
+
+# (The table's radix-15 row -- kernel residual 9e-12 for a single application -- is a kernel
+# fitted to S_15 itself; the residual-framework radix-15 kernel of the library carries its
+# designed spillover (0.185 B^15, ...), so one application of it gives 0.8546 instead of 0.860:
+# not the same kernel, not pinned here.)
+
+
+def test_table_approx_radix33_printed_polynomial(oracle_lib):
+    # radix-33 row: inverse error 0.722, "vs Exact" 1.007, from the printed 2-decimal
+    # coefficients evaluated by C-2's coefficient (Horner) mode; the rounding of the printed
+    # coefficients moves the error by < 0.002
+    B, Ainv = _approx_table_matrix()
+    Y = O.plan_apply(B, [33], np.eye(64), coeffs=[[F(str(c)) for c in _R33_PRINTED]])
+    err = _inv_err(Y, Ainv)
+    exact = _inv_err(O.series_sum(B, 33, np.eye(64))[0], Ainv)
+    assert abs(err - 0.722) < 2e-3
+    assert 1.0 < err / exact < 1.01
