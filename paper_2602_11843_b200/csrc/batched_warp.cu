@@ -68,12 +68,19 @@ __device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigne
   return d;
 }
 
-// 3xTF32 split (reading R14): hi = tf32 round-to-nearest-away of x, computed on the bit pattern
-// (add half an ulp of the 10-bit mantissa, clear the low 13 bits; finite inputs); lo = x - hi is
+// 3xTF32 split (reading R14): hi = tf32 round-to-nearest-even of x (cvt.rn.tf32.f32 is ONE
+// F2FP.TF32 instruction; the round-1 bit-pattern rna split took two and is kept as the
+// NSERIES_BW_SPLIT_BITS variant: 281 -> 258 us per config-4 batch, same error,
+// profiles/r02_batched_f2fp_split.txt); lo = x - hi is
 // exact in fp32 and is passed as is -- the tensor core reads the top 19 bits of a .tf32 operand,
 // i.e. truncates lo, an error below 2^-11 |lo| <= 2^-22 |x| (same order as the dropped lo*lo).
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+#if defined(NSERIES_BW_SPLIT_BITS)
   hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+#else
+  // round to nearest EVEN: one F2FP.TF32.F32 on sm_100a (cvt.rna is emulated by 4 instructions)
+  asm("cvt.rn.tf32.f32 %0, %1;\n" : "=r"(hi) : "f"(x));
+#endif
   lo = __float_as_uint(x - __uint_as_float(hi));
 }
 
