@@ -7,7 +7,7 @@
 // traffic is therefore the algorithmic minimum, 2 d^2 elements per matrix.
 //
 //   fp32: mma.sync m16n8k8 .tf32 with a 3xTF32 split done in registers at fragment load
-//         (hi = cvt.rna.tf32(x), lo = cvt.rna.tf32(x - hi); acc += lo*hi + hi*lo + hi*hi),
+//         (hi = cvt.rn.tf32(x), lo = cvt.rn.tf32(x - hi); acc += lo*hi + hi*lo + hi*hi),
 //         fp32 accumulation (reading R14).
 //   fp64: mma.sync m8n8k4 .f64 (DMMA).
 // Matrices are zero-padded to DP (multiple of 16) inside shared memory; gamma*I is applied
@@ -22,15 +22,15 @@ namespace nseries {
 
 namespace {
 
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
+__device__ __forceinline__ uint32_t tf32_rn(float x) {   // one F2FP.TF32 (round to nearest even)
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  asm("cvt.rn.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return r;
 }
 
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = tf32_rna(x);
-  lo = tf32_rna(x - __uint_as_float(hi));
+  hi = tf32_rn(x);
+  lo = tf32_rn(x - __uint_as_float(hi));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {

@@ -1,7 +1,7 @@
 // gemm_tf32.cu -- FP32 engine: 3xTF32 products on the 5th-generation tensor cores (sm_100a).
 //
 // acc = X * Y (d x d x d) with fp32 accuracy from three tcgen05.mma .kind::tf32 passes
-//   acc = Xhi*Yhi + (Xhi*Ylo + Xlo*Yhi)        (hi = rna_tf32(x), lo = rna_tf32(x - hi))
+//   acc = Xhi*Yhi + (Xhi*Ylo + Xlo*Yhi)        (hi = rn_tf32(x), lo = rn_tf32(x - hi), round to nearest even)
 // Operands live in HBM as tf32 "planes" (hi and lo, fp32 containers, leading dimension ldp,
 // a multiple of 32) written by the producing epilogue (or by the one-off split of the user's
 // A), so the mainloop is pure TMA -> SMEM -> tcgen05 with no conversion work (DESIGN.md
@@ -303,16 +303,12 @@ __device__ __forceinline__ void fadd2(float& a0, float& a1, float x, float y) {
   a1 = __uint_as_float((uint32_t)(uc >> 32));
 }
 
-__device__ __forceinline__ float rna_tf32(float x) {
+// tf32 round to nearest even: cvt.rn.tf32.f32 is ONE F2FP.TF32 instruction on sm_100a
+// (cvt.rna is emulated by 4, the rna bit-pattern trick takes 2; tools/f2fp_split.cu)
+__device__ __forceinline__ float rn_tf32(float x) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  asm("cvt.rn.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
-}
-
-// tf32 round-to-nearest-away on the bit pattern (same result as cvt.rna.tf32.f32, incl. inf and
-// NaN; 2 instructions instead of 4)
-__device__ __forceinline__ float rna_tf32_fast(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 #ifdef NSERIES_TF32_DEBUG
@@ -339,8 +335,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Misaligned or ragged quads (d % 4 != 0, tile edges) take a scalar path with the same formulas.
 __device__ __forceinline__ float4 ld4g(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ float q4(const float4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
-__device__ __forceinline__ float4 rna4(const float4& v) {
-  return make_float4(rna_tf32_fast(v.x), rna_tf32_fast(v.y), rna_tf32_fast(v.z), rna_tf32_fast(v.w));
+__device__ __forceinline__ float4 rn4(const float4& v) {
+  return make_float4(rn_tf32(v.x), rn_tf32(v.y), rn_tf32(v.z), rn_tf32(v.w));
 }
 __device__ __forceinline__ float4 sub4(const float4& a, const float4& b) {
   return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
@@ -481,9 +477,9 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
             if (dq == 3) t.w += ga[o];
             if (ox[o]) st_quad(ox[o] + (size_t)r * old_[o] + hn0, qc, t, smask, vec);
             if (oh[o]) {
-              const float4 hi = rna4(t);
+              const float4 hi = rn4(t);
               st_quad(oh[o] + (size_t)r * ldp + hn0, qc, hi, smask, vec);
-              st_quad(ol[o] + (size_t)r * ldp + hn0, qc, rna4(sub4(t, hi)), smask, vec);
+              st_quad(ol[o] + (size_t)r * ldp + hn0, qc, rn4(sub4(t, hi)), smask, vec);
             }
             if (o == tout) *reinterpret_cast<float4*>(vt + rr * kStageLd + qc) = t;
           }
@@ -513,9 +509,9 @@ __device__ __forceinline__ void tile_epilogue(const uint32_t tiles_off, const in
             const float val = q4(v, e);
             if (tx) tx[(size_t)c * tld + r] = val;
             if (th) {
-              const float hi = rna_tf32_fast(val);
+              const float hi = rn_tf32(val);
               th[(size_t)c * ldp + r] = hi;
-              tl[(size_t)c * ldp + r] = rna_tf32_fast(val - hi);
+              tl[(size_t)c * ldp + r] = rn_tf32(val - hi);
             }
           }
         }
@@ -828,7 +824,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mXh, const __grid_constan
     // ring is idle: every MMA has completed and every stage was consumed).  Staging tiles
     // [128][EC+1] (acc, then the output value); the +1 pad keeps row- and column-wise
     // accesses conflict-free.  All per-output parameters are hoisted into registers (the
-    // pass is instruction-bound), tf32 splits use the 2-instruction bit-pattern rna.
+    // pass is instruction-bound), tf32 splits are one F2FP each (cvt.rn).
     // both column halves are staged at once (the accumulator registers die here); the
     // current output's values go to a third staging tile for the transposed column pass
     float* const tiles = reinterpret_cast<float*>(smem_raw + (reinterpret_cast<uint8_t*>(&sm.xh[0][0]) - smem_raw));
@@ -933,8 +929,8 @@ __global__ void split_planes_kernel(const float* __restrict__ x, int ld_in, floa
       float h = 0.f, l = 0.f;
       if (r < d && c < d) {
         const float v = identity ? (r == c ? 1.f : 0.f) : x[(size_t)r * ld_in + c];
-        h = rna_tf32(v);
-        l = rna_tf32(v - h);
+        h = rn_tf32(v);
+        l = rn_tf32(v - h);
         if (hi) { hi[(size_t)r * ld_out + c] = h; lo[(size_t)r * ld_out + c] = l; }
       }
       th[i][threadIdx.x] = h;
@@ -963,7 +959,7 @@ __global__ void axpby_f32_kernel(int d, const __grid_constant__ EpiParamsF32 ep)
       for (int x = 0; x < ep.n_aux; ++x) t = fma(ep.beta[o][x], (double)ep.aux[x][(size_t)r * ep.aux_ld[x] + c], t);
       if (r == c) t += ep.gamma[o];
       const float v = (float)t;
-      const float h = rna_tf32(v), l = rna_tf32(v - h);
+      const float h = rn_tf32(v), l = rn_tf32(v - h);
       if (ep.out_x[o]) ep.out_x[o][(size_t)r * ep.out_ld[o] + c] = v;
       if (ep.out_hi[o]) { ep.out_hi[o][(size_t)r * ep.ldp + c] = h; ep.out_lo[o][(size_t)r * ep.ldp + c] = l; }
       if (ep.out_hiT[o]) { ep.out_hiT[o][(size_t)c * ep.ldp + r] = h; ep.out_loT[o][(size_t)c * ep.ldp + r] = l; }
