@@ -1060,10 +1060,10 @@ static nseries_status eval_batched_impl(nseries_handle h, const void* A, int64_t
   const Program& P = it->second;
   if ((int)P.ops.size() > kMaxBatchedOps) return NSERIES_ERR_UNSUPPORTED_SIZE;
   const bool check = (flags & NSERIES_CHECK_FINITE) != 0;
-  if (dt == NSERIES_F32 && d <= 32) {
-    WarpProgram wp{};
-    nseries_status wst = build_warp_program(P, &wp);
-    if (wst != NSERIES_OK) return wst;
+  WarpProgram wp{};
+  nseries_status wst = (dt == NSERIES_F32 && d <= 32) ? build_warp_program(P, &wp) : NSERIES_ERR_UNSUPPORTED_SIZE;
+  if (wst != NSERIES_OK && wst != NSERIES_ERR_UNSUPPORTED_SIZE) return wst;
+  if (wst == NSERIES_OK) {   // else: the CTA-per-matrix kernel below
     h->stats = nseries_stats{};
     h->stats.products = h->stats.products_exec = P.products;
     h->stats.products_paper = paper_products(p);

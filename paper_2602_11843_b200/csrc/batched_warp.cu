@@ -75,6 +75,10 @@ __device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigne
 // exact in fp32 and is passed as is -- the tensor core reads the top 19 bits of a .tf32 operand,
 // i.e. truncates lo, an error below 2^-11 |lo| <= 2^-22 |x| (same order as the dropped lo*lo).
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+#if defined(NSERIES_BW_NOSPLIT)   // timing experiment only (wrong numerics): no split instructions
+  hi = lo = __float_as_uint(x);
+  return;
+#endif
 #if defined(NSERIES_BW_SPLIT_BITS)
   hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
 #else
@@ -148,24 +152,51 @@ struct __align__(16) DevOp {
 };
 constexpr uint16_t kNoOff = 0xffff;
 
-// This warp's part of X * Y into registers: rows 0..31 (2 m16 tiles) x column tiles
-// nb0 .. nb0+NBW-1 (n8 tiles).  XI / YI: operand is the identity (synthesised, zero outside
-// the d x d block).
+#ifdef NSERIES_BW_TIMING   // harness-only (tools/bw_probe.cu): per-phase clocks summed over warps
+__device__ unsigned long long g_bwt[4];   // mainloop, barrier 1, epilogue, barrier 2
+#define BW_T(i) const long long bwt##i = clock64()
+#define BW_TACC tacc[0] += bwt1 - bwt0; tacc[1] += bwt2 - bwt1; tacc[2] += bwt3 - bwt2; tacc[3] += bwt4 - bwt3
+#define BW_TPARAM , long long (&tacc)[4]
+#define BW_TARG , tacc
+#else
+#define BW_T(i) ((void)0)
+#define BW_TACC ((void)0)
+#define BW_TPARAM
+#define BW_TARG
+#endif
+
+// Row-block order: warp w of a 2-warp group walks its two m16 row blocks in the order
+// mb = lm ^ w (lm = 0, 1), so the tiles holding diagonal elements are (lm = 0, j = hh) for both
+// warps -- a compile-time fact in the epilogue (WPM = 1: j = 2 lm + hh with lm = mb).  WPM = 4
+// keeps mb = lm and tests the diagonal at run time.
+template <int WPM>
+__device__ __forceinline__ int row_swap(int wig) { return WPM == 2 ? wig : 0; }
+template <int WPM>
+__device__ __forceinline__ bool diag_tile(int lm, int j, int hh, int nb0) {
+  if (WPM == 2) return lm == 0 && j == hh;
+  if (WPM == 1) return j == 2 * lm + hh;
+  return nb0 + j == 2 * lm + hh;
+}
+
+// This warp's part of X * Y into registers: rows 0..31 (2 m16 tiles, local index lm = mb ^ msw)
+// x column tiles nb0 .. nb0+NBW-1 (n8 tiles).  XI / YI: operand is the identity (synthesised,
+// zero outside the d x d block); its tf32 lo part is exactly zero, so that cross product is not
+// issued (the product is still the full 3xTF32 product: the skipped term is 0).
 template <int NBW, bool XI, bool YI>
-__device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, int g, int t, int nb0,
+__device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, int g, int t, int nb0, int msw,
                                          float (&big)[2][NBW][4], float (&sml)[2][NBW][4]) {
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     const int k0 = 8 * s + 2 * t;   // this lane's k pair in k-step s: k0 (slot t), k0+1 (slot t+4)
-    float2 xa[2][2];                // [mb][hh]: X[16 mb + 8 hh + g][k0 .. k0+1]
+    float2 xa[2][2];                // [lm][hh]: X[16 (lm ^ msw) + 8 hh + g][k0 .. k0+1]
     float yb[NBW][2];               // [j][e]:  Y[k0 + e][8 (nb0 + j) + g]
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+    for (int lm = 0; lm < 2; ++lm)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        const int r = 16 * mb + 8 * hh + g;
-        if (XI) xa[mb][hh] = make_float2((r == k0 && r < d) ? 1.f : 0.f, (r == k0 + 1 && r < d) ? 1.f : 0.f);
-        else xa[mb][hh] = *reinterpret_cast<const float2*>(X + swz(r, k0));
+        const int r = 16 * (lm ^ msw) + 8 * hh + g;
+        if (XI) xa[lm][hh] = make_float2((r == k0 && r < d) ? 1.f : 0.f, (r == k0 + 1 && r < d) ? 1.f : 0.f);
+        else xa[lm][hh] = *reinterpret_cast<const float2*>(X + 512 * (lm ^ msw) + swz(8 * hh + g, k0));
       }
 #pragma unroll
     for (int j = 0; j < NBW; ++j)
@@ -177,87 +208,110 @@ __device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, 
       }
     uint32_t ah[2][2][2], al[2][2][2], bh[NBW][2], bl[NBW][2];
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+    for (int lm = 0; lm < 2; ++lm)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        split_tf32(xa[mb][hh].x, ah[mb][hh][0], al[mb][hh][0]);
-        split_tf32(xa[mb][hh].y, ah[mb][hh][1], al[mb][hh][1]);
+        if (XI) {   // 0 / 1 are exact tf32 values
+          ah[lm][hh][0] = __float_as_uint(xa[lm][hh].x);
+          ah[lm][hh][1] = __float_as_uint(xa[lm][hh].y);
+        } else {
+          split_tf32(xa[lm][hh].x, ah[lm][hh][0], al[lm][hh][0]);
+          split_tf32(xa[lm][hh].y, ah[lm][hh][1], al[lm][hh][1]);
+        }
       }
 #pragma unroll
     for (int j = 0; j < NBW; ++j)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) split_tf32(yb[j][e], bh[j][e], bl[j][e]);
+      for (int e = 0; e < 2; ++e) {
+        if (YI) bh[j][e] = __float_as_uint(yb[j][e]);
+        else split_tf32(yb[j][e], bh[j][e], bl[j][e]);
+      }
     // issue order: the three products of a k-step run over all tiles before an accumulator is
     // reused; fragment a = {(g, t), (g+8, t), (g, t+4), (g+8, t+4)}, b = {t, t+4}
+    if (!XI) {
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+      for (int lm = 0; lm < 2; ++lm)
 #pragma unroll
-      for (int j = 0; j < NBW; ++j) {
-        if (s == 0) mma_tf32_z(sml[mb][j], al[mb][0][0], al[mb][1][0], al[mb][0][1], al[mb][1][1], bh[j][0], bh[j][1]);
-        else mma_tf32(sml[mb][j], al[mb][0][0], al[mb][1][0], al[mb][0][1], al[mb][1][1], bh[j][0], bh[j][1]);
-      }
+        for (int j = 0; j < NBW; ++j) {
+          if (s == 0) mma_tf32_z(sml[lm][j], al[lm][0][0], al[lm][1][0], al[lm][0][1], al[lm][1][1], bh[j][0], bh[j][1]);
+          else mma_tf32(sml[lm][j], al[lm][0][0], al[lm][1][0], al[lm][0][1], al[lm][1][1], bh[j][0], bh[j][1]);
+        }
+    }
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+    for (int lm = 0; lm < 2; ++lm)
 #pragma unroll
       for (int j = 0; j < NBW; ++j) {
 #if defined(NSERIES_BW_CHAIN_BIG)
-        if (s == 0) mma_tf32_z(big[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
-        else mma_tf32(big[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
+        if (s == 0) mma_tf32_z(big[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
+        else mma_tf32(big[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
 #else
         // hi*hi of each k-step from a zero accumulator, summed in fp32 registers with IEEE
         // round-to-nearest adds: a chained tensor-core accumulator truncates at every k-step
         // (profiles/r01_tf32_accumulation_probe.txt), which biases the dominant term; the
         // cross terms (2^-11 smaller) stay chained
         if (s == 0) {
-          mma_tf32_z(big[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
+          mma_tf32_z(big[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
         } else {
           float tk[4];
-          mma_tf32_z(tk, ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bh[j][0], bh[j][1]);
-          const unsigned long long p01 = add2(pk(big[mb][j][0], big[mb][j][1]), pk(tk[0], tk[1]));
-          const unsigned long long p23 = add2(pk(big[mb][j][2], big[mb][j][3]), pk(tk[2], tk[3]));
-          big[mb][j][0] = __uint_as_float((uint32_t)p01);
-          big[mb][j][1] = __uint_as_float((uint32_t)(p01 >> 32));
-          big[mb][j][2] = __uint_as_float((uint32_t)p23);
-          big[mb][j][3] = __uint_as_float((uint32_t)(p23 >> 32));
+          mma_tf32_z(tk, ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
+          const unsigned long long p01 = add2(pk(big[lm][j][0], big[lm][j][1]), pk(tk[0], tk[1]));
+          const unsigned long long p23 = add2(pk(big[lm][j][2], big[lm][j][3]), pk(tk[2], tk[3]));
+          big[lm][j][0] = __uint_as_float((uint32_t)p01);
+          big[lm][j][1] = __uint_as_float((uint32_t)(p01 >> 32));
+          big[lm][j][2] = __uint_as_float((uint32_t)p23);
+          big[lm][j][3] = __uint_as_float((uint32_t)(p23 >> 32));
         }
 #endif
       }
+    if (!YI) {
 #pragma unroll
-    for (int mb = 0; mb < 2; ++mb)
+      for (int lm = 0; lm < 2; ++lm)
 #pragma unroll
-      for (int j = 0; j < NBW; ++j)
-        mma_tf32(sml[mb][j], ah[mb][0][0], ah[mb][1][0], ah[mb][0][1], ah[mb][1][1], bl[j][0], bl[j][1]);
+        for (int j = 0; j < NBW; ++j) {
+          if (XI && s == 0) mma_tf32_z(sml[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bl[j][0], bl[j][1]);
+          else mma_tf32(sml[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bl[j][0], bl[j][1]);
+        }
+    }
   }
 }
 
-// Epilogue out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I on the accumulator registers,
-// outputs to shared-memory slots (every op but the one producing the final S).  Pairs of
-// columns (2t, 2t+1) are processed as packed fp32x2.
+// Epilogue out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I on the accumulator registers.
+// Outputs go to their shared-memory slots; with FIN (the op producing the final S, once per
+// matrix) outputs flagged in gmask also go to global memory (8-byte stores when vec_out) and
+// NSERIES_CHECK_FINITE counts their NaN/Inf entries.  Pairs of columns (2t, 2t+1) are
+// processed as packed fp32x2.  gamma_j I is added on the diagonal tiles only (diag_tile);
+// diagonal positions of the zero padding beyond d get it too: values stay block-diagonal
+// (the padding block carries the scalar series at 0), and nothing beyond d is stored or read
+// into the d x d block.
 typedef unsigned long long u64;
-template <int NBW, int NA, int NO>
-__device__ __forceinline__ void warp_epilogue(const DevOp& op, float* ws, int d, int g, int t,
-                                              int nb0, const float (&big)[2][NBW][4],
-                                              const float (&sml)[2][NBW][4]) {
+template <int WPM, int NBW, int NA, int NO, bool FIN>
+__device__ __forceinline__ void warp_epilogue(const DevOp& op, float* ws, float* Sg, int d, bool vec_out, int g,
+                                              int t, int nb0, int msw, const float (&big)[2][NBW][4],
+                                              const float (&sml)[2][NBW][4], int* nonfinite) {
   const float* auxp[NA > 0 ? NA : 1];
   float* outp[NO];
   u64 alpha[NO], beta[NO][NA > 0 ? NA : 1];
   float gamma[NO];
+  bool to_slot[NO], to_g[NO];
+  const bool dg0 = (g == 2 * t), dg1 = (g == 2 * t + 1);
 #pragma unroll
   for (int x = 0; x < NA; ++x) auxp[x] = ws + op.aux[x];
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
-    outp[o] = ws + op.out[o];
+    to_slot[o] = !FIN || op.out[o] != kNoOff;
+    to_g[o] = FIN && (op.gmask & (1 << o));
+    outp[o] = ws + (to_slot[o] ? op.out[o] : 0);
     alpha[o] = pk(op.alpha[o], op.alpha[o]);
     gamma[o] = op.gamma[o];
 #pragma unroll
     for (int x = 0; x < NA; ++x) beta[o][x] = pk(op.beta[o][x], op.beta[o][x]);
   }
-  // diagonal elements of this lane: tiles (mb, nb, hh) with nb == 2 mb + hh, row g, cols 2t, 2t+1
-  const bool dg0 = (g == 2 * t), dg1 = (g == 2 * t + 1);
+  int nonfin = 0;
   // Batches of 2*NBW column pairs: every aux load of a batch is issued before its first store
   // (an output may overwrite an aux slot in place, so the compiler cannot reorder them itself).
 #pragma unroll
-  for (int mb = 0; mb < 2; ++mb) {
+  for (int lm = 0; lm < 2; ++lm) {
+    const int rb = 16 * (lm ^ msw);
     u64 av[NBW][2][NA > 0 ? NA : 1];
 #pragma unroll
     for (int j = 0; j < NBW; ++j)
@@ -265,65 +319,27 @@ __device__ __forceinline__ void warp_epilogue(const DevOp& op, float* ws, int d,
       for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
         for (int x = 0; x < NA; ++x)
-          av[j][hh][x] = *reinterpret_cast<const u64*>(auxp[x] + swz(16 * mb + 8 * hh + g, 8 * (nb0 + j) + 2 * t));
+          av[j][hh][x] = *reinterpret_cast<const u64*>(auxp[x] + 32 * rb + swz(8 * hh + g, 8 * (nb0 + j) + 2 * t));
 #pragma unroll
     for (int j = 0; j < NBW; ++j)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        const int nb = nb0 + j;
-        const int r = 16 * mb + 8 * hh + g, c = 8 * nb + 2 * t;
-        const int off = swz(r, c);
-        const u64 acc = add2(pk(big[mb][j][2 * hh], big[mb][j][2 * hh + 1]),
-                             pk(sml[mb][j][2 * hh], sml[mb][j][2 * hh + 1]));
-        const bool diag = (nb == 2 * mb + hh) && r < d;   // only these tiles hold diagonal elements
+        const int r = rb + 8 * hh + g, c = 8 * (nb0 + j) + 2 * t;
+        const int off = 32 * rb + swz(8 * hh + g, c);
+        const u64 acc = add2(pk(big[lm][j][2 * hh], big[lm][j][2 * hh + 1]),
+                             pk(sml[lm][j][2 * hh], sml[lm][j][2 * hh + 1]));
+        const bool diag = diag_tile<WPM>(lm, j, hh, nb0);
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
           u64 v = mul2(alpha[o], acc);
 #pragma unroll
           for (int x = 0; x < NA; ++x) v = fma2(beta[o][x], av[j][hh][x], v);
           if (diag) v = add2(v, pk(dg0 ? gamma[o] : 0.f, dg1 ? gamma[o] : 0.f));
-          *reinterpret_cast<u64*>(outp[o] + off) = v;
-        }
-      }
-  }
-}
-
-// Generic epilogue for the op producing the final S (once per matrix): outputs with gmask go to
-// global memory (and to their slot if they are read later).
-template <int NBW>
-__device__ __forceinline__ void warp_epilogue_final(const DevOp& op, float* ws, float* Sg, int d,
-                                                    bool vec_out, int g, int t, int nb0,
-                                                    const float (&big)[2][NBW][4], const float (&sml)[2][NBW][4],
-                                                    int* nonfinite) {
-  int nonfin = 0;   // NSERIES_CHECK_FINITE: NaN/Inf entries of the final S
-#pragma unroll
-  for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-    for (int j = 0; j < NBW; ++j)
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int r = 16 * mb + 8 * hh + g, c = 8 * (nb0 + j) + 2 * t;
-        const int off = swz(r, c);
-        const float acc0 = big[mb][j][2 * hh] + sml[mb][j][2 * hh];
-        const float acc1 = big[mb][j][2 * hh + 1] + sml[mb][j][2 * hh + 1];
-        float2 av[kMaxAux];
-#pragma unroll
-        for (int x = 0; x < kMaxAux; ++x)
-          av[x] = x < (op.epi >> 2) ? *reinterpret_cast<const float2*>(ws + op.aux[x] + off) : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int o = 0; o < kMaxOut; ++o) {
-          if (o >= (op.epi & 3)) break;
-          float v0 = op.alpha[o] * acc0, v1 = op.alpha[o] * acc1;
-#pragma unroll
-          for (int x = 0; x < kMaxAux; ++x) {   // beta = 0 beyond n_aux
-            v0 = fmaf(op.beta[o][x], av[x].x, v0);
-            v1 = fmaf(op.beta[o][x], av[x].y, v1);
-          }
-          if (r == c && r < d) v0 += op.gamma[o];
-          if (r == c + 1 && r < d) v1 += op.gamma[o];
-          if (op.out[o] != kNoOff) *reinterpret_cast<float2*>(ws + op.out[o] + off) = make_float2(v0, v1);
-          if (op.gmask & (1 << o)) {
-            nonfin += ((r < d && c < d && !isfinite(v0)) ? 1 : 0) + ((r < d && c + 1 < d && !isfinite(v1)) ? 1 : 0);
+          if (to_slot[o]) *reinterpret_cast<u64*>(outp[o] + off) = v;
+          if (FIN && to_g[o]) {
+            const float v0 = __uint_as_float((uint32_t)v), v1 = __uint_as_float((uint32_t)(v >> 32));
+            if (nonfinite)
+              nonfin += ((r < d && c < d && !isfinite(v0)) ? 1 : 0) + ((r < d && c + 1 < d && !isfinite(v1)) ? 1 : 0);
             if (vec_out) {
               *reinterpret_cast<float2*>(Sg + r * 32 + c) = make_float2(v0, v1);
             } else if (r < d) {
@@ -333,7 +349,8 @@ __device__ __forceinline__ void warp_epilogue_final(const DevOp& op, float* ws, 
           }
         }
       }
-  if (nonfinite) {
+  }
+  if (FIN && nonfinite) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nonfin += __shfl_xor_sync(0xffffffffu, nonfin, o);
     if (((threadIdx.x & 31) == 0) && nonfin) atomicAdd(nonfinite, nonfin);
@@ -343,24 +360,41 @@ __device__ __forceinline__ void warp_epilogue_final(const DevOp& op, float* ws, 
 // One fused op for the group's matrix (this warp's column tiles).
 template <int WPM>
 __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, int d, bool vec_out, int g, int t,
-                                        int nb0, int group, int* nonfinite) {
+                                        int nb0, int msw, int group, int* nonfinite BW_TPARAM) {
   constexpr int NBW = 4 / WPM;
   float big[2][NBW][4], sml[2][NBW][4];
   const int kind = op.kind;
-  if (kind == 1) warp_mma<NBW, false, false>(ws + op.x, ws + op.y, d, g, t, nb0, big, sml);
-  else if (kind == 2) warp_mma<NBW, true, false>(ws, ws + op.y, d, g, t, nb0, big, sml);
-  else if (kind == 3) warp_mma<NBW, false, true>(ws + op.x, ws, d, g, t, nb0, big, sml);
-  else {
+  BW_T(0);
+  if (kind == 1) warp_mma<NBW, false, false>(ws + op.x, ws + op.y, d, g, t, nb0, msw, big, sml);
+  else if (kind == 2) warp_mma<NBW, true, false>(ws, ws + op.y, d, g, t, nb0, msw, big, sml);
+  else if (kind == 3) warp_mma<NBW, false, true>(ws + op.x, ws, d, g, t, nb0, msw, big, sml);
+  else {   // axpby op (rare: elided binary plans, k = 1): acc = 0.  The zeros are volatile
+           // moves so ptxas cannot hoist 16 CS2R above the kind branch into every product.
 #pragma unroll
     for (int mb = 0; mb < 2; ++mb)
 #pragma unroll
       for (int j = 0; j < NBW; ++j)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) big[mb][j][e] = sml[mb][j][e] = 0.f;
+        for (int e = 0; e < 4; ++e) {
+          asm volatile("mov.b32 %0, 0;\n" : "=f"(big[mb][j][e]));
+          asm volatile("mov.b32 %0, 0;\n" : "=f"(sml[mb][j][e]));
+        }
   }
+#ifdef NSERIES_BW_TIMING
+  {   // wait for the accumulators so the mainloop time includes the last HMMAs
+    float z = 0.f;
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int j = 0; j < NBW; ++j) z += big[mb][j][0] + sml[mb][j][0];
+    if (z == 1.2345e-30f) Sg[0] = z;
+  }
+#endif
+  BW_T(1);
   NSERIES_SHAKE_POINT(8 * kind + 1);
   group_sync<WPM>(group);   // every operand read of the group precedes any output write (in-place slots)
   NSERIES_SHAKE_POINT(8 * kind + 2);
+  BW_T(2);
 #if defined(NSERIES_BW_PROBE) && NSERIES_BW_PROBE == 1   // tools/bw_probe.cu: mainloop only
   {
     float sum = 0.f;
@@ -373,20 +407,32 @@ __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, i
     return;
   }
 #endif
-  if (op.gmask) {
-    warp_epilogue_final<NBW>(op, ws, Sg, d, vec_out, g, t, nb0, big, sml, nonfinite);
-  } else switch (op.epi) {
-#define NSERIES_EPI(NA, NO) \
-  case NA * 4 + NO: warp_epilogue<NBW, NA, NO>(op, ws, d, g, t, nb0, big, sml); break;
+  const int sel = op.epi + (op.gmask ? 16 : 0);
+  switch (sel) {
+#define NSERIES_EPI(NA, NO)                                                                          \
+  case NA * 4 + NO:                                                                                  \
+    warp_epilogue<WPM, NBW, NA, NO, false>(op, ws, Sg, d, vec_out, g, t, nb0, msw, big, sml, nonfinite); \
+    break;
+#define NSERIES_FIN(NA, NO)                                                                          \
+  case 16 + NA * 4 + NO:                                                                             \
+    warp_epilogue<WPM, NBW, NA, NO, true>(op, ws, Sg, d, vec_out, g, t, nb0, msw, big, sml, nonfinite);  \
+    break;
     NSERIES_EPI(0, 1) NSERIES_EPI(0, 2) NSERIES_EPI(0, 3)
     NSERIES_EPI(1, 1) NSERIES_EPI(1, 2) NSERIES_EPI(1, 3)
     NSERIES_EPI(2, 1) NSERIES_EPI(2, 2) NSERIES_EPI(2, 3)
     NSERIES_EPI(3, 1) NSERIES_EPI(3, 2) NSERIES_EPI(3, 3)
+    // the op producing the final S has at most 2 aux / 2 outputs in every compiled plan
+    // (build_warp_program refuses others; the 3-aux / 3-output final variants would spill)
+    NSERIES_FIN(0, 1) NSERIES_FIN(0, 2) NSERIES_FIN(1, 1) NSERIES_FIN(1, 2) NSERIES_FIN(2, 1) NSERIES_FIN(2, 2)
+#undef NSERIES_FIN
 #undef NSERIES_EPI
     default: break;
   }
+  BW_T(3);
   NSERIES_SHAKE_POINT(8 * kind + 3);
   group_sync<WPM>(group);
+  BW_T(4);
+  BW_TACC;
 }
 
 // One CTA per SM holding up to 8 groups (one copy of the decoded op list per CTA); register
@@ -400,6 +446,7 @@ batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const floa
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int group = warp / WPM, wig = warp % WPM, groups = (blockDim.x >> 5) / WPM;
   const int g = lane >> 2, t = lane & 3, glane = wig * 32 + lane, nb0 = wig * (4 / WPM);
+  const int msw = row_swap<WPM>(wig);
   // decoded op list, two copies (A in buffer 0 / buffer 1), ahead of the groups' slots
   DevOp* sops = reinterpret_cast<DevOp*>(smem_f);
   for (int i = threadIdx.x; i < 2 * prog.n_ops; i += blockDim.x) {
@@ -436,6 +483,9 @@ batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const floa
   auto srcp = [&](int b) -> const float* { return A_ptrs ? A_ptrs[b] : A + (int64_t)b * strideA; };
   auto vec_ok = [&](const void* p) { return d == 32 && ((uintptr_t)p & 15) == 0; };
   int cur = 0;
+#ifdef NSERIES_BW_TIMING
+  long long tacc[4] = {0, 0, 0, 0};
+#endif
 #ifdef NSERIES_BW_PROBE
   if (prog.probe_delay_ns && blockIdx.x * 2 >= gridDim.x) __nanosleep(prog.probe_delay_ns);
 #endif
@@ -458,10 +508,15 @@ batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const floa
     float* Sg = S_ptrs ? S_ptrs[b] : S + (int64_t)b * strideS;
     const bool vec_out = d == 32 && ((uintptr_t)Sg & 7) == 0;
     const DevOp* ops = sops + cur * prog.n_ops;
-    for (int o = 0; o < prog.n_ops; ++o) warp_op<WPM>(ops[o], ws, Sg, d, vec_out, g, t, nb0, group, nonfinite);
+    for (int o = 0; o < prog.n_ops; ++o)
+      warp_op<WPM>(ops[o], ws, Sg, d, vec_out, g, t, nb0, msw, group, nonfinite BW_TARG);
     cur ^= 1;
   }
   cp_async_wait<0>();
+#ifdef NSERIES_BW_TIMING
+  if (lane == 0)
+    for (int i = 0; i < 4; ++i) atomicAdd(&g_bwt[i], (unsigned long long)tacc[i]);
+#endif
 }
 
 template <int WPM>
@@ -538,6 +593,8 @@ nseries_status build_warp_program(const Program& P, WarpProgram* out, bool inpla
       }
     }
   }
+  for (int i = 0; i < wp.n_ops; ++i)   // final-S epilogues are instantiated up to 2 aux / 2 outputs
+    if (wp.ops[i].gmask && (wp.ops[i].n_aux > 2 || wp.ops[i].n_out > 2)) return NSERIES_ERR_UNSUPPORTED_SIZE;
   return NSERIES_OK;
 }
 

@@ -1,6 +1,8 @@
 // Harness-only probe of the batched warp kernel (config 4 shape, 16384 x 32^2 fp32, x9x9 plan):
 // builds the real op list through the library's host code and times the kernel compiled with
-// -DNSERIES_BW_PROBE=0 (full) or 1 (mainloop only, epilogues replaced by a sink).
+// -DNSERIES_BW_PROBE=0 (full) or 1 (mainloop only, epilogues replaced by a sink); with
+// -DNSERIES_BW_TIMING also the clock64 time per phase of a warp-op (mainloop incl. the last
+// HMMAs, group barrier, epilogue, group barrier).
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -32,6 +34,17 @@ int main(int argc, char** argv) {
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("probe %d delay %u wpm %d: %.1f us (%s)\n", NSERIES_BW_PROBE, delay, wpm, ms / 20 * 1e3, cudaGetErrorString(cudaGetLastError()));
+#ifdef NSERIES_BW_TIMING
+    {   // per-phase clocks per warp-op, averaged (one extra launch with the counters zeroed)
+      unsigned long long z[4] = {0, 0, 0, 0}, r[4];
+      cudaMemcpyToSymbol(g_bwt, z, sizeof(z));
+      launch_batched_warp_f32(A, d * d, nullptr, S, d * d, nullptr, batch, d, wp, 0);
+      cudaMemcpyFromSymbol(r, g_bwt, sizeof(r));
+      const double n = (double)batch * wp.n_ops * wpm;   // warp-ops
+      printf("  clk per warp-op: mainloop %.0f  barrier1 %.0f  epilogue %.0f  barrier2 %.0f\n",
+             r[0] / n, r[1] / n, r[2] / n, r[3] / n);
+    }
+#endif
   }
   return 0;
 }
