@@ -168,7 +168,8 @@ __device__ unsigned long long g_bwt[4];   // mainloop, barrier 1, epilogue, barr
 // Row-block order: warp w of a 2-warp group walks its two m16 row blocks in the order
 // mb = lm ^ w (lm = 0, 1), so the tiles holding diagonal elements are (lm = 0, j = hh) for both
 // warps -- a compile-time fact in the epilogue (WPM = 1: j = 2 lm + hh with lm = mb).  WPM = 4
-// keeps mb = lm and tests the diagonal at run time.
+// keeps mb = lm and tests the diagonal at run time.  (Natural row order with a run-time
+// mb == w predicate measured slower: 254 -> 260 us, profiles/r02_batched_diag_ab.txt.)
 template <int WPM>
 __device__ __forceinline__ int row_swap(int wig) { return WPM == 2 ? wig : 0; }
 template <int WPM>
@@ -182,9 +183,21 @@ __device__ __forceinline__ bool diag_tile(int lm, int j, int hh, int nb0) {
 // x column tiles nb0 .. nb0+NBW-1 (n8 tiles).  XI / YI: operand is the identity (synthesised,
 // zero outside the d x d block); its tf32 lo part is exactly zero, so that cross product is not
 // issued (the product is still the full 3xTF32 product: the skipped term is 0).
+__device__ __forceinline__ void add_acc(float (&b)[4], const float (&t)[4]) {   // b += t, IEEE RN
+  const unsigned long long p01 = add2(pk(b[0], b[1]), pk(t[0], t[1]));
+  const unsigned long long p23 = add2(pk(b[2], b[3]), pk(t[2], t[3]));
+  b[0] = __uint_as_float((uint32_t)p01);
+  b[1] = __uint_as_float((uint32_t)(p01 >> 32));
+  b[2] = __uint_as_float((uint32_t)p23);
+  b[3] = __uint_as_float((uint32_t)(p23 >> 32));
+}
+
 template <int NBW, bool XI, bool YI>
 __device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, int g, int t, int nb0, int msw,
                                          float (&big)[2][NBW][4], float (&sml)[2][NBW][4]) {
+#if !defined(NSERIES_BW_CHAIN_BIG)
+  float tk[2][NBW][4];   // hi*hi of the previous k-step, added one k-step late
+#endif
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     const int k0 = 8 * s + 2 * t;   // this lane's k pair in k-step s: k0 (slot t), k0+1 (slot t+4)
@@ -252,14 +265,12 @@ __device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, 
         if (s == 0) {
           mma_tf32_z(big[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
         } else {
-          float tk[4];
-          mma_tf32_z(tk, ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
-          const unsigned long long p01 = add2(pk(big[lm][j][0], big[lm][j][1]), pk(tk[0], tk[1]));
-          const unsigned long long p23 = add2(pk(big[lm][j][2], big[lm][j][3]), pk(tk[2], tk[3]));
-          big[lm][j][0] = __uint_as_float((uint32_t)p01);
-          big[lm][j][1] = __uint_as_float((uint32_t)(p01 >> 32));
-          big[lm][j][2] = __uint_as_float((uint32_t)p23);
-          big[lm][j][3] = __uint_as_float((uint32_t)(p23 >> 32));
+          // the k-step's hi*hi sum is added one k-step later, so the FADD2 does not wait on the
+          // HMMA just issued (same summation order ((s0 + s1) + s2) + s3, bit-identical results;
+          // 258 -> 254 us per config-4 batch, profiles/r02_batched_lag_add.txt)
+          if (s >= 2) add_acc(big[lm][j], tk[lm][j]);
+          mma_tf32_z(tk[lm][j], ah[lm][0][0], ah[lm][1][0], ah[lm][0][1], ah[lm][1][1], bh[j][0], bh[j][1]);
+          if (s == 3) add_acc(big[lm][j], tk[lm][j]);
         }
 #endif
       }
