@@ -43,10 +43,16 @@ namespace {
 
 constexpr int kSlotF = 1024;   // floats per 32 x 32 slot
 
+#if defined(NSERIES_BW_QSWZ)
+// (SIMT control experiment) 4-float quads XOR-swizzled by row (r & 7): a warp's row-quad loads
+// of 8 rows hit 32 distinct banks, but the epilogue's pair accesses become 2-way conflicted
+__device__ __forceinline__ int swz(int r, int c) { return r * 32 + (((c >> 2) ^ (r & 7)) << 2) + (c & 3); }
+#else
 __device__ __forceinline__ int swz(int r, int c) {
   const int h = ((r ^ (r >> 2)) & 1) | (r & 2);
   return r * 32 + (((c >> 3) ^ h) << 3) + (c & 7);
 }
+#endif
 
 // packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2 on sm_100a), IEEE round-to-nearest
 __device__ __forceinline__ unsigned long long pk(float x, float y) {
@@ -192,6 +198,76 @@ __device__ __forceinline__ void add_acc(float (&b)[4], const float (&t)[4]) {   
   b[3] = __uint_as_float((uint32_t)(p23 >> 32));
 }
 
+#if defined(NSERIES_BW_FFMA)
+// CONTROL VARIANT (harness-only, tools/variants): the same fragment outputs computed with SIMT
+// fp32 FMAs (packed FFMA2, one fp32 product instead of three tf32 ones): the lane's 4 rows x
+// 2 column pairs form a 4x4 outer-product block; X quads by LDS.128, Y pairs by LDS.64.
+template <int NBW, bool XI, bool YI>
+__device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, int g, int t, int nb0, int msw,
+                                         float (&big)[2][NBW][4], float (&sml)[2][NBW][4]) {
+#pragma unroll
+  for (int lm = 0; lm < 2; ++lm)
+#pragma unroll
+    for (int j = 0; j < NBW; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sml[lm][j][e] = 0.f;
+  if (XI || YI) {   // I * Y = Y, X * I = X at the fragment positions (zero outside d x d)
+    const float* V = XI ? Y : X;
+#pragma unroll
+    for (int lm = 0; lm < 2; ++lm)
+#pragma unroll
+      for (int j = 0; j < NBW; ++j)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float2 v = *reinterpret_cast<const float2*>(V + 512 * (lm ^ msw) + swz(8 * hh + g, 8 * (nb0 + j) + 2 * t));
+          big[lm][j][2 * hh] = v.x;
+          big[lm][j][2 * hh + 1] = v.y;
+        }
+    return;
+  }
+  unsigned long long acc[2][NBW][2];
+#pragma unroll
+  for (int lm = 0; lm < 2; ++lm)
+#pragma unroll
+    for (int j = 0; j < NBW; ++j) acc[lm][j][0] = acc[lm][j][1] = 0ull;
+#ifndef NSERIES_BW_FFMA_UNROLL
+#define NSERIES_BW_FFMA_UNROLL 2
+#endif
+  constexpr int kFfmaUnroll = NSERIES_BW_FFMA_UNROLL;   // (pragma arguments are not macro-expanded)
+#pragma unroll kFfmaUnroll
+  for (int q = 0; q < 8; ++q) {   // k = 4q .. 4q+3
+    float4 xq[2][2];
+#pragma unroll
+    for (int lm = 0; lm < 2; ++lm)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        xq[lm][hh] = *reinterpret_cast<const float4*>(X + 512 * (lm ^ msw) + swz(8 * hh + g, 4 * q));
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      unsigned long long yp[NBW];
+#pragma unroll
+      for (int j = 0; j < NBW; ++j) yp[j] = *reinterpret_cast<const unsigned long long*>(Y + swz(4 * q + kk, 8 * (nb0 + j) + 2 * t));
+#pragma unroll
+      for (int lm = 0; lm < 2; ++lm)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const float xv = kk == 0 ? xq[lm][hh].x : kk == 1 ? xq[lm][hh].y : kk == 2 ? xq[lm][hh].z : xq[lm][hh].w;
+#pragma unroll
+          for (int j = 0; j < NBW; ++j) acc[lm][j][hh] = fma2(pk(xv, xv), yp[j], acc[lm][j][hh]);
+        }
+    }
+  }
+#pragma unroll
+  for (int lm = 0; lm < 2; ++lm)
+#pragma unroll
+    for (int j = 0; j < NBW; ++j)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        big[lm][j][2 * hh] = __uint_as_float((uint32_t)acc[lm][j][hh]);
+        big[lm][j][2 * hh + 1] = __uint_as_float((uint32_t)(acc[lm][j][hh] >> 32));
+      }
+}
+#else
 template <int NBW, bool XI, bool YI>
 __device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, int g, int t, int nb0, int msw,
                                          float (&big)[2][NBW][4], float (&sml)[2][NBW][4]) {
@@ -285,6 +361,8 @@ __device__ __forceinline__ void warp_mma(const float* X, const float* Y, int d, 
     }
   }
 }
+
+#endif   // NSERIES_BW_FFMA
 
 // Epilogue out_j = alpha_j acc + sum_i beta_ji aux_i + gamma_j I on the accumulator registers.
 // Outputs go to their shared-memory slots; with FIN (the op producing the final S, once per
