@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-plan", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs 1/2/4 side lines")
+    ap.add_argument("--sharded-direct", action="store_true",
+                    help="with --sharded: read right factors in place from the peers' arenas (CUDA IPC "
+                         "over NVLink, NSERIES_SHARDED_DIRECT) instead of an allgather per product")
     ap.add_argument("--sharded", action="store_true",
                     help="NEXT-3: config 5 (d = 8192, k = 10000) row-sharded across the N ranks "
                          "(strong scaling; not the headline line)")
@@ -476,6 +479,15 @@ def other_configs(P, h, stream):
         "overhead_vs_dense": ms8 / ms - 1.0,
         "note": "all row blocks on one GPU; an 8-rank run executes 1/8 of these launches per GPU plus "
                 "NCCL allgather-v gathers (not measurable on this 1-GPU box)"}
+    # the same with NSERIES_SHARDED_DIRECT: right factors read in place from the 8 row blocks
+    msd = _time_evals(lambda: P.nseries_eval_sharded(h, As, 0, n, 8192, 10000, plan=plan, S_shards=Ss,
+                                                     flags=fl | P.NSERIES_SHARDED_DIRECT, stream=stream),
+                      1, 1, stream)
+    st = P.nseries_last_stats(h)
+    out["next3_sharded_cfg5_8blocks_1gpu_direct"] = {
+        "blocks": n, "ms_per_eval": msd, "gathers": st["gathers"], "overhead_vs_dense": msd / ms - 1.0,
+        "note": "NSERIES_SHARDED_DIRECT: each GEMM's k-tile loads read the right factor's row blocks in "
+                "place (no gather, no full copy)"}
     del A, As, Ss
     return out
 
@@ -556,6 +568,13 @@ def run_sharded(args):
     S_blk = torch.empty_like(A_blk)
     fl = P.NSERIES_ALLOW_APPROX
     plan = P.nseries_plan_build(k, P.NSERIES_PLAN_AUTO, [15, 9, 5, 2], fl)
+    if args.sharded_direct:
+        # right factors read in place from the owners' arenas over NVLink (CUDA IPC), one-int
+        # all-reduce barrier per op, instead of an allgather per product
+        from paper_2602_11843_b200 import replicas
+        fl |= P.NSERIES_SHARDED_DIRECT
+        need = P.nseries_sharded_arena_bytes(d, world, 1, k, plan, flags=fl)
+        P.nseries_peer_import(h, replicas.exchange_blobs(P.nseries_peer_export(h, need), world))
     stream = torch.cuda.current_stream()
     run = lambda: P.nseries_eval_sharded(h, [A_blk], rank, world, d, k, plan=plan, S_shards=[S_blk], flags=fl,
                                          stream=stream)
@@ -587,6 +606,8 @@ def run_sharded(args):
                                            "products": plan.products, "parallelism": f"row-shard{world}"},
             "tflops": tf, "frac_of_fp64_peak_per_gpu": tf / world / FP64_PEAK_TFLOPS,
             "gathers": st["gathers"], "gathers_prefetched": st["gathers_prefetched"],
+            "right_factors": "in place over NVLink (NSERIES_SHARDED_DIRECT)" if args.sharded_direct
+            else "NCCL allgather-v per product",
             "nccl_log": "stderr (NCCL_DEBUG=INFO, SUBSYS=INIT)"}))
     P.nseries_destroy(h)
     return 0

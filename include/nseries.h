@@ -107,6 +107,18 @@ typedef enum {
                                          (stats.nonfinite).  SURVEY F5: config 4's divergent
                                          matrices (rho > 1) overflow fp32 for large k.      */
 
+#define NSERIES_SHARDED_DIRECT   0x100u/* nseries_eval_sharded: read the right factor of every
+                                         product in place, straight from its row blocks (the GEMM's
+                                         k-tile loads pick the block that holds rows k0..k0+BK),
+                                         instead of gathering it into a full buffer first.  Needs
+                                         every block of the factor addressable by this process:
+                                         all shards local (one GPU), or the peers' arenas mapped
+                                         with nseries_peer_import; uniform blocks (d divisible by
+                                         nshards, rows a multiple of 32, nshards <= 16).  Factors
+                                         that are not addressable (the user's A or S blocks of a
+                                         peer) are still gathered.  Falls back to gathers where
+                                         the conditions do not hold.                          */
+
 #define NSERIES_MAX_STEPS 128
 
 /* A plan: a sequence of steps from n = 1 to n = k.  step[i] = m in 2..32 multiplies n by m;
@@ -266,6 +278,30 @@ nseries_status nseries_matmul(nseries_handle h, nseries_dtype dt, const void* X,
  *   product counts as nseries_eval (NSERIES_SYMMETRIC is rejected); eager launches (no
  *   graph).  stats.launches counts GEMM/axpby launches, stats.gathers the gathers. */
 nseries_status nseries_shard_rows(int32_t d, int32_t nshards, int32_t shard, int32_t* row0, int32_t* rows);
+
+/* ---- in-place right factors across GPUs (NSERIES_SHARDED_DIRECT with a communicator) ------
+ * SURVEY.md 8(f) NEXT-3 "TMA-over-NVLink" variant: instead of an allgather of the right factor
+ * before every product, each GEMM's k-tile loads read the factor's row blocks where they live
+ * -- in the owning rank's arena, mapped into this process over NVLink by CUDA IPC -- and a
+ * one-int ncclAllReduce after every op is the barrier that orders the owners' writes before
+ * the readers' loads (and the loads before the next overwrite).
+ * nseries_sharded_arena_bytes: host-only, pure: the arena size one rank needs for this plan
+ *   (n_local x (value slots + 1 copy of A) x rows_max x d doubles).
+ * nseries_peer_export: allocate (or grow to `bytes`; every rank must pass the same size) this
+ *   handle's arena -- a plain cudaMalloc allocation; synchronizes the device -- and write its
+ *   64-byte cudaIpcMemHandle_t to handle_out.
+ * nseries_peer_import: `handles` holds nranks consecutive 64-byte handles indexed by rank (the
+ *   caller all-gathers them over any side channel); maps every peer's arena
+ *   (cudaIpcOpenMemHandle, P2P access enabled lazily), this rank's own entry is skipped.  Needs
+ *   nseries_comm_init first with the same nranks.  Afterwards nseries_eval_sharded with
+ *   NSERIES_SHARDED_DIRECT and a matching shard map reads right factors in place (the user's S
+ *   / R blocks of peers are still gathered).  Handles mapped until nseries_destroy or the next
+ *   import / a growing export. */
+nseries_status nseries_sharded_arena_bytes(int32_t d, int32_t nshards, int32_t n_local, int64_t k,
+                                          const nseries_plan* plan, uint32_t flags, int32_t want_R,
+                                          uint64_t* bytes);
+nseries_status nseries_peer_export(nseries_handle h, uint64_t bytes, void* handle_out /* 64 bytes */);
+nseries_status nseries_peer_import(nseries_handle h, const void* handles /* nranks x 64 bytes */, int32_t nranks);
 nseries_status nseries_comm_unique_id(void* id_out /* 128 bytes */);
 nseries_status nseries_comm_init(nseries_handle h, const void* id /* 128 bytes */, int32_t nranks, int32_t rank);
 nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shards, int32_t n_local,

@@ -25,6 +25,7 @@ NSERIES_SYNC_STATS = 0x10
 NSERIES_SYMMETRIC = 0x20
 NSERIES_HOST_ASYNC = 0x40
 NSERIES_CHECK_FINITE = 0x80
+NSERIES_SHARDED_DIRECT = 0x100
 NSERIES_MAX_STEPS = 128
 
 # every symbol include/nseries.h declares (tests check the .so exports exactly these)
@@ -34,6 +35,7 @@ EXPORTED = [
     "nseries_eval_host", "nseries_eval_batched_strided", "nseries_eval_batched",
     "nseries_matmul", "nseries_last_stats", "nseries_solve", "nseries_shard_rows",
     "nseries_comm_unique_id", "nseries_comm_init", "nseries_eval_sharded", "nseries_host_sync",
+    "nseries_sharded_arena_bytes", "nseries_peer_export", "nseries_peer_import",
 ]
 
 
@@ -113,6 +115,10 @@ def load_library(path=None):
         "nseries_comm_init": ([vp, vp, i32, i32], ctypes.c_int),
         "nseries_eval_sharded": ([vp, ctypes.POINTER(vp), i32, i32, i32, i32, i64, plan_p, ctypes.c_int,
                                   ctypes.POINTER(vp), ctypes.POINTER(vp), u32, vp], ctypes.c_int),
+        "nseries_sharded_arena_bytes": ([i32, i32, i32, i64, plan_p, u32, i32, ctypes.POINTER(ctypes.c_uint64)],
+                                        ctypes.c_int),
+        "nseries_peer_export": ([vp, ctypes.c_uint64, vp], ctypes.c_int),
+        "nseries_peer_import": ([vp, vp, i32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -286,6 +292,32 @@ def nseries_comm_init(h, uid, nranks, rank):
         raise ValueError("NCCL unique id must be 128 bytes")
     buf = ctypes.create_string_buffer(bytes(uid), 128)
     _check(load_library().nseries_comm_init(h, buf, int(nranks), int(rank)), "nseries_comm_init")
+
+
+def nseries_sharded_arena_bytes(d, nshards, n_local, k, plan=None, flags=0, want_R=False):
+    """Arena bytes one rank needs for NSERIES_SHARDED_DIRECT across processes (host-only)."""
+    b = ctypes.c_uint64()
+    _check(load_library().nseries_sharded_arena_bytes(int(d), int(nshards), int(n_local), int(k),
+                                                      ctypes.byref(plan) if plan is not None else None,
+                                                      int(flags), int(bool(want_R)), ctypes.byref(b)),
+           "nseries_sharded_arena_bytes")
+    return b.value
+
+
+def nseries_peer_export(h, nbytes):
+    """Allocate / grow the handle's arena to nbytes; returns its 64-byte CUDA IPC handle."""
+    buf = ctypes.create_string_buffer(64)
+    _check(load_library().nseries_peer_export(h, ctypes.c_uint64(int(nbytes)), buf), "nseries_peer_export")
+    return buf.raw
+
+
+def nseries_peer_import(h, handles):
+    """Map the peers' arenas: `handles` = list of 64-byte IPC handles indexed by rank."""
+    blob = b"".join(bytes(x) for x in handles)
+    if any(len(x) != 64 for x in handles):
+        raise ValueError("IPC handles are 64 bytes")
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(load_library().nseries_peer_import(h, buf, len(handles)), "nseries_peer_import")
 
 
 def nseries_eval_sharded(h, A_shards, first_shard, nshards, d, k, plan=None, S_shards=None, R_shards=None,

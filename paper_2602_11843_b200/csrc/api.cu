@@ -67,6 +67,14 @@ struct nseries_ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_evaldone[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   cudaStream_t last_eval_stream = nullptr;
   cudaStream_t gather_stream = nullptr;      // prefetching gathers run here
+  // NSERIES_SHARDED_DIRECT across processes: this rank's arena (plain cudaMalloc, exported by
+  // CUDA IPC) holding the row blocks of every value, the peers' arenas mapped over NVLink
+  // (index = rank; own entry = arena), and a 1-int buffer the per-op barrier all-reduces
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  std::vector<void*> peer_arena;
+  int* bar_dev = nullptr;
+  cudaEvent_t ev_bar = nullptr;
   cudaEvent_t ev_gready = nullptr, ev_gdone[3] = {nullptr, nullptr, nullptr};
   // NSERIES_CHECK_FINITE: device counter of NaN/Inf entries of S and its pinned host copy;
   // nf_active is set while an eval with the flag enqueues its ops (engines that count in
@@ -436,6 +444,7 @@ struct NcclApi {
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
 };
 NcclApi load_nccl() {
   NcclApi api;
@@ -450,8 +459,9 @@ NcclApi load_nccl() {
       api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(lib, "ncclGroupStart"));
       api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(lib, "ncclGroupEnd"));
       api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(lib, "ncclGetErrorString"));
+      api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(lib, "ncclAllReduce"));
       api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.broadcast && api.group_start &&
-               api.group_end && api.error_string;
+               api.group_end && api.error_string && api.all_reduce;
     }
   }
   return api;
@@ -480,7 +490,7 @@ void shard_range(int d, int n, int s, int* row0, int* rows) {
 // (rows x d) x (d x d) with its identity terms offset by the block's first row.
 nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const* A_sh, double* const* S_sh,
                            double* const* R_sh, int n_local, int first, int nshards, int d, cudaStream_t s,
-                           int* launches, int* gathers, int* prefetched) {
+                           bool want_direct, int* launches, int* gathers, int* prefetched) {
   // over NCCL whenever the handle's communicator matches the shard map (with one rank the
   // broadcasts are all local: the single-GPU test of the collective path); else device copies
   const bool remote = h->comm && nshards == h->nranks * n_local && first == h->rank * n_local;
@@ -496,9 +506,36 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
   double* const A_full = static_cast<double*>(h->full);
   double* const G[2] = {A_full + dd, A_full + 2 * dd};
   double* const ident = static_cast<double*>(h->ident);
+  // NSERIES_SHARDED_DIRECT: a product reads its right factor in place from the factor's row
+  // blocks (the GEMM's k-tile loads pick the block; no gather, no full copy) when every block
+  // is addressable here and the blocks are uniform.  Single process: all shards local.  Across
+  // processes (direct_mr): every value's blocks live in the ranks' arenas at the same offsets
+  // (per local shard: n_slots value slots + a copy of A), the peers' arenas are mapped over
+  // NVLink (nseries_peer_import), and an all-reduce of one int after every op is the barrier
+  // that orders a rank's writes before the peers' reads (and the reads before the next write).
+  const bool uniform = nshards <= kMaxShards && d % nshards == 0 && (d / nshards) % 32 == 0;
+  const int slots_per = P.n_slots + 1;
+  const size_t arena_need = (size_t)n_local * slots_per * ((size_t)rows_max * d) * sizeof(double);
+  const bool direct_mr = want_direct && remote && uniform && h->arena && h->bar_dev &&
+                         (int)h->peer_arena.size() == h->nranks && h->arena_bytes >= arena_need;
+  const bool direct = (want_direct && !remote && n_local == nshards && uniform) || direct_mr;
+  double* const arena = static_cast<double*>(h->arena);
+  // block of value v in the arena based at `base` (local shard index jl of its owner)
+  auto arena_blk = [&](double* base, int v, int jl) -> double* {
+    const int slot_idx = P.val_kind[v] == V_USER_A ? P.n_slots : P.val_buf[v];
+    return base + ((size_t)jl * slots_per + slot_idx) * slot;
+  };
+  auto addressable = [&](int v) {
+    if (!direct) return false;
+    const int kd = P.val_kind[v];
+    if (kd == V_USER_R && R_sh == nullptr) return false;
+    if (direct_mr && (kd == V_USER_S || kd == V_USER_R)) return h->nranks == 1;   // peers' user blocks: gathered
+    return true;
+  };
   // row block j (local index) of value v
   auto blk = [&](int v, int j) -> double* {
     const int g = first + j;
+    if (direct_mr && (P.val_kind[v] == V_USER_A || P.val_kind[v] == V_TEMP)) return arena_blk(arena, v, j);
     switch (P.val_kind[v]) {
       case V_USER_A: return const_cast<double*>(A_sh[j]);
       case V_IDENT: return ident + (size_t)row0[g] * d;
@@ -552,6 +589,43 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
     }
     return cuda_fail(h, cudaEventRecord(h->ev_gdone[b], gs));
   };
+  // block of value v owned by shard g, wherever it lives (direct modes): this process's block,
+  // or -- direct_mr -- the same arena offset in the owner's mapped arena
+  auto any_blk = [&](int v, int g) -> const double* {
+    const int owner = g / n_local, jl = g - owner * n_local;
+    if (!direct_mr || owner == h->rank) return blk(v, g - first);
+    if (P.val_kind[v] == V_IDENT) return ident + (size_t)row0[g] * d;
+    return arena_blk(static_cast<double*>(h->peer_arena[owner]), v, jl);
+  };
+  // cross-rank barrier of direct_mr: a one-int all-reduce on the gather stream (the only
+  // stream that carries this communicator's collectives), event-ordered with s on both sides
+  auto barrier = [&]() -> nseries_status {
+    cudaError_t e = cudaEventRecord(h->ev_gready, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(gs, h->ev_gready, 0);
+    if (e != cudaSuccess) return cuda_fail(h, e);
+    nseries_status st = nccl_fail(h, nccl().all_reduce(h->bar_dev, h->bar_dev, 1, ncclInt32, ncclSum, h->comm, gs));
+    if (st != NSERIES_OK) return st;
+    e = cudaEventRecord(h->ev_bar, gs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->ev_bar, 0);
+    return cuda_fail(h, e);
+  };
+  if (direct_mr) {
+    if (!h->ev_bar) {
+      cudaError_t e = cudaEventCreateWithFlags(&h->ev_bar, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(h, e);
+    }
+    // the peers may still read this arena (last op of their previous eval): meet first; then
+    // A's local blocks go into the arena, and nobody reads a peer's A before every copy landed
+    nseries_status st = barrier();
+    for (int j = 0; j < n_local && st == NSERIES_OK; ++j) {
+      const int aval = [&] { for (int v = 0; v < P.n_values; ++v) if (P.val_kind[v] == V_USER_A) return v; return -1; }();
+      if (aval < 0) break;
+      st = cuda_fail(h, cudaMemcpyAsync(arena_blk(arena, aval, j), A_sh[j], (size_t)rows[first + j] * d * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, s));
+    }
+    if (st == NSERIES_OK) st = barrier();
+    if (st != NSERIES_OK) return st;
+  }
   // producer op of every value (-1: A, I or never produced)
   std::vector<int> producer(P.n_values, -1);
   for (size_t i = 0; i < P.ops.size(); ++i)
@@ -564,6 +638,7 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
   int cached[2] = {-1, -1}, lru = 0;          // lru: the buffer to overwrite next
   bool pending[3] = {false, false, false};    // gathers into G[0], G[1], A_full not yet awaited on s
   auto cost = [&](int v) {
+    if (addressable(v)) return 0;
     const int kd = P.val_kind[v];
     if (kd == V_IDENT) return 0;
     if (kd == V_USER_A) return a_full ? 0 : 1;
@@ -615,12 +690,15 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
     int left = op.X, right = op.Y;
     const double* Yf = nullptr;
     int cur_buf = -1;
+    const bool in_place = op.gemm && addressable(op.X) && addressable(op.Y);
     if (op.gemm) {
       right = right_of(op);
       left = right == op.X ? op.Y : op.X;
-      nseries_status st = full_of(right, &Yf);
-      if (st != NSERIES_OK) return st;
-      cur_buf = Yf == G[0] ? 0 : (Yf == G[1] ? 1 : -1);
+      if (!in_place) {
+        nseries_status st = full_of(right, &Yf);
+        if (st != NSERIES_OK) return st;
+        cur_buf = Yf == G[0] ? 0 : (Yf == G[1] ? 1 : -1);
+      }
     }
     // prefetch: the next product's gathered factor, if it exists before this op runs, into
     // the buffer this op does not read (the previous op's reads are ordered by the event)
@@ -655,9 +733,18 @@ nseries_status run_sharded(nseries_ctx* h, const Program& P, const double* const
         ep.gamma[o] = op.gamma[o];
         for (int a = 0; a < kMaxAux; ++a) ep.beta[o][a] = op.beta[o][a];
       }
+      if (in_place) {   // every block of the right factor, in row order (no output aliases it:
+                        // the op list never writes an operand's buffer in the same op)
+        ep.yrows = rows[0];
+        for (int g2 = 0; g2 < nshards; ++g2) ep.yblk[g2] = any_blk(right, g2);
+      }
       const int rc = op.gemm ? launch_gemm_f64(blk(left, j), Yf, d, ep, s) : launch_axpby_f64(d, ep, s);
       if (rc != 0) return cuda_fail(h, (cudaError_t)rc);
       ++nl;
+    }
+    if (direct_mr && i + 1 < P.ops.size()) {   // this op's blocks written everywhere before any peer reads them
+      nseries_status st = barrier();
+      if (st != NSERIES_OK) return st;
     }
   }
   for (int b = 0; b < 3; ++b) {                 // the caller's stream owns everything at exit
@@ -730,6 +817,11 @@ nseries_status nseries_destroy(nseries_handle h) {
   if (h->full) cudaFree(h->full);
   if (h->comm && nccl().ok) nccl().comm_destroy(h->comm);
   if (h->ident) cudaFree(h->ident);
+  for (size_t r = 0; r < h->peer_arena.size(); ++r)
+    if ((int)r != h->rank && h->peer_arena[r]) cudaIpcCloseMemHandle(h->peer_arena[r]);
+  if (h->arena) cudaFree(h->arena);
+  if (h->bar_dev) cudaFree(h->bar_dev);
+  if (h->ev_bar) cudaEventDestroy(h->ev_bar);
   if (h->stage) cudaFree(h->stage);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -1327,6 +1419,74 @@ nseries_status nseries_comm_unique_id(void* id_out) {
   return NSERIES_OK;
 }
 
+nseries_status nseries_sharded_arena_bytes(int32_t d, int32_t nshards, int32_t n_local, int64_t k,
+                                          const nseries_plan* plan, uint32_t flags, int32_t want_R,
+                                          uint64_t* bytes) {
+  if (!bytes || d < 1 || nshards < 1 || n_local < 1 || n_local > nshards || d < nshards || k < 1)
+    return NSERIES_ERR_INVALID_ARG;
+  nseries_plan p;
+  nseries_status st = resolve_plan(plan, k, flags, &p);
+  if (st != NSERIES_OK) return st;
+  Program prog;
+  st = compile_plan(p, want_R != 0, &prog);
+  if (st != NSERIES_OK) return st;
+  const size_t rows_max = (size_t)(d + nshards - 1) / nshards;
+  *bytes = (uint64_t)n_local * (prog.n_slots + 1) * rows_max * d * sizeof(double);
+  return NSERIES_OK;
+}
+
+nseries_status nseries_peer_export(nseries_handle h, uint64_t bytes, void* handle_out) {
+  if (!h || !handle_out || bytes == 0) return NSERIES_ERR_INVALID_ARG;
+  if (h->sticky != NSERIES_OK) return h->sticky;
+  cudaSetDevice(h->device);
+  cudaError_t e = cudaDeviceSynchronize();   // setup call: nothing may still use an old arena
+  if (e == cudaSuccess && h->arena_bytes < bytes) {
+    for (size_t r = 0; r < h->peer_arena.size(); ++r)
+      if ((int)r != h->rank && h->peer_arena[r]) cudaIpcCloseMemHandle(h->peer_arena[r]);
+    h->peer_arena.clear();
+    if (h->arena) cudaFree(h->arena);
+    h->arena = nullptr;
+    h->arena_bytes = 0;
+    e = cudaMalloc(&h->arena, bytes);   // plain allocation: pool (cudaMallocAsync) memory is not IPC-exportable
+    if (e == cudaSuccess) h->arena_bytes = bytes;
+  }
+  if (e == cudaSuccess && !h->bar_dev) {
+    e = cudaMalloc(&h->bar_dev, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(h->bar_dev, 0, sizeof(int));
+  }
+  cudaIpcMemHandle_t ih;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&ih, h->arena);
+  if (e != cudaSuccess) return cuda_fail(h, e);
+  std::memcpy(handle_out, &ih, sizeof(ih));
+  return NSERIES_OK;
+}
+
+nseries_status nseries_peer_import(nseries_handle h, const void* handles, int32_t nranks) {
+  if (!h || !handles || nranks < 1) return NSERIES_ERR_INVALID_ARG;
+  if (h->sticky != NSERIES_OK) return h->sticky;
+  if (!h->comm || nranks != h->nranks || !h->arena) return NSERIES_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  for (size_t r = 0; r < h->peer_arena.size(); ++r)
+    if ((int)r != h->rank && h->peer_arena[r]) cudaIpcCloseMemHandle(h->peer_arena[r]);
+  h->peer_arena.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == h->rank) {
+      h->peer_arena[r] = h->arena;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, static_cast<const char*>(handles) + (size_t)r * sizeof(ih), sizeof(ih));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      h->peer_arena.clear();
+      return cuda_fail(h, e);
+    }
+    h->peer_arena[r] = ptr;
+  }
+  return NSERIES_OK;
+}
+
 nseries_status nseries_comm_init(nseries_handle h, const void* id, int32_t nranks, int32_t rank) {
   if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks) return NSERIES_ERR_INVALID_ARG;
   if (h->sticky != NSERIES_OK) return h->sticky;
@@ -1395,8 +1555,8 @@ nseries_status nseries_eval_sharded(nseries_handle h, const void* const* A_shard
   if (timing) cudaEventRecord(h->ev0, s);
   int launches = 0, gathers = 0, prefetched = 0;
   st = run_sharded(h, P, reinterpret_cast<const double* const*>(A_shards), reinterpret_cast<double* const*>(S_shards),
-                   reinterpret_cast<double* const*>(R_shards), n_local, first_shard, nshards, d, s, &launches,
-                   &gathers, &prefetched);
+                   reinterpret_cast<double* const*>(R_shards), n_local, first_shard, nshards, d, s,
+                   (flags & NSERIES_SHARDED_DIRECT) != 0, &launches, &gathers, &prefetched);
   if (st != NSERIES_OK) return st;
   mark_use(h, s);
   if (check) {   // this process's row blocks of S

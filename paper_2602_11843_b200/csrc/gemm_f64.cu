@@ -105,6 +105,15 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
   const int wm0 = (warp / C::kWarpsN) * WM, wn0 = (warp % C::kWarpsN) * WN;
   const int g = lane >> 2, t = lane & 3;
 
+  // row k0 of the right factor: Y itself, or (NSERIES_SHARDED_DIRECT) inside the row block that
+  // holds rows k0 .. k0+BK-1 (one integer division per k-tile)
+  auto y_rows = [&](int k0) -> const double* {
+    if (ep.yrows > 0) {
+      const int sh = k0 / ep.yrows;
+      return ep.yblk[sh] + (size_t)(k0 - sh * ep.yrows) * d;
+    }
+    return Y + (size_t)k0 * d;
+  };
   auto load_stage = [&](int stage, int kt) {
     const int k0 = kt * BK;
     double* a = sA + stage * C::kStageA;
@@ -119,13 +128,14 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
         bool ok = gr < M && gc < d;
         cp_async16(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok);
       }
+      const double* Yk = y_rows(k0);   // row k0 of Y (in place: inside its row block)
       constexpr int kChunksB = BK * BN / 2;
 #pragma unroll
       for (int q = tid; q < kChunksB; q += C::kThreads) {
         int r = q / (BN / 2), c = (q % (BN / 2)) * 2;
         int gr = k0 + r, gc = n0 + c;
         bool ok = gr < d && gc < d;
-        cp_async16(b + r * C::kLdB + c, ok ? Y + (size_t)gr * d + gc : Y, ok);
+        cp_async16(b + r * C::kLdB + c, ok ? Yk + (size_t)r * d + gc : Yk, ok);
       }
     } else {
 #pragma unroll 4
@@ -135,12 +145,13 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
         bool ok = gr < M && gc < d;
         cp_async8(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok);
       }
+      const double* Yk = y_rows(k0);
 #pragma unroll 4
       for (int q = tid; q < BK * BN; q += C::kThreads) {
         int r = q / BN, c = q % BN;
         int gr = k0 + r, gc = n0 + c;
         bool ok = gr < d && gc < d;
-        cp_async8(b + r * C::kLdB + c, ok ? Y + (size_t)gr * d + gc : Y, ok);
+        cp_async8(b + r * C::kLdB + c, ok ? Yk + (size_t)r * d + gc : Yk, ok);
       }
     }
   };
@@ -385,6 +396,10 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   bool v2 = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) % 16 == 0);
   for (int i = 0; i < ep.n_aux; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.aux[i]) % 16 == 0;
   for (int i = 0; i < ep.n_out; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.out[i]) % 16 == 0;
+  if (ep.yrows > 0) {
+    if (ep.sym || ep.yrows % 32 != 0 || (d + ep.yrows - 1) / ep.yrows > kMaxShards) return (int)cudaErrorInvalidValue;
+    for (int i = 0; i < (d + ep.yrows - 1) / ep.yrows; ++i) v2 = v2 && reinterpret_cast<uintptr_t>(ep.yblk[i]) % 16 == 0;
+  }
   // Tile choice: 32x32 for small whole matrices (below), else by modelled efficiency 128x128
   // (1 CTA/SM) vs 64x64 (2 CTAs/SM) over 148 SMs (NSERIES_F64_TILE = 1 / 3 / 4 forces one,
   // harness only).

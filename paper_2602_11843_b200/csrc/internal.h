@@ -95,6 +95,7 @@ inline int smem_attr_once(int bytes) {
 #endif
 
 // ---------------------------------------------------------------- device engines
+constexpr int kMaxShards = 16;   // row blocks a directly-read right factor may span
 struct EpiParams {
   int n_aux, n_out;
   const void* aux[kMaxAux];
@@ -111,6 +112,10 @@ struct EpiParams {
   int row0 = 0;                  // (0: rows = d) starting at global row row0 (I's diagonal offset)
   int* nonfinite = nullptr;      // NSERIES_CHECK_FINITE: count NaN/Inf entries of out[nf_out]
   int nf_out = -1;
+  // NSERIES_SHARDED_DIRECT: the right factor Y is read in place from row blocks of yrows rows
+  // (yrows > 0, a multiple of every BK, so a k-tile never straddles two blocks)
+  int yrows = 0;
+  const double* yblk[kMaxShards] = {};
 };
 // NSERIES_CHECK_FINITE on paths without a fused count: NaN/Inf entries of a (batch of) rows x d S
 int launch_count_nonfinite(nseries_dtype dt, const void* S, int64_t stride, const void* const* S_ptrs, int batch,

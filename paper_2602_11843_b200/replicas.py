@@ -77,6 +77,17 @@ def gather_counts(local, world, device="cpu"):
     return [int(x.item()) for x in out]
 
 
+def exchange_blobs(blob, world):
+    """All ranks' byte strings, indexed by rank (e.g. the 64-byte CUDA IPC handles of
+    nseries_peer_export, which nseries_peer_import takes in rank order)."""
+    if world <= 1:
+        return [bytes(blob)]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, bytes(blob))
+    return out
+
+
 def teardown(world):
     if world > 1:
         import torch.distributed as dist

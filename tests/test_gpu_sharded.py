@@ -2,8 +2,9 @@
 nseries_eval_sharded): the plan evaluated on row blocks with a gathered right factor per
 product must match the single-matrix engine to rounding (the row split changes which CTA
 computes an element, not its K loop, but the executor may take X.Y as Y.X to avoid a gather,
-which reorders the rounding) and the oracle.  Covers all-local shards (device-copy gathers) and the NCCL allgather-v path with a
-one-rank communicator (grouped ncclBroadcast, every root local)."""
+which reorders the rounding) and the oracle.  Covers all-local shards (device-copy gathers), the
+NCCL allgather-v path with a one-rank communicator (grouped ncclBroadcast, every root local) and
+NSERIES_SHARDED_DIRECT (right factors read in place from their row blocks, no gather)."""
 import numpy as np
 import pytest
 import torch
@@ -128,6 +129,96 @@ def test_sharded_config3():
         assert st["gathers"] == 14 and st["gathers_prefetched"] == 2
     finally:
         P.nseries_destroy(hh)
+
+
+@pytest.mark.parametrize("d,n", [(256, 1), (256, 2), (256, 8), (96, 3), (1024, 8)])
+@pytest.mark.parametrize("steps", [[9, 9], [15, 15], [2] * 6, [15, 1, 5], [5, 1, 9], [3, 3]])
+def test_sharded_direct(h, d, n, steps):
+    # NSERIES_SHARDED_DIRECT: every right factor read in place from its row blocks -- no gather
+    A = torch.from_numpy(inputs.random_matrix(d, 700 + d + n, 0.8)).cuda()
+    S, _, st = _sharded(h, A, steps, n, extra=P.NSERIES_SHARDED_DIRECT)
+    Sd, _ = _dense(h, A, steps)
+    assert O.rel_fro(S, Sd) <= 1e-13, (d, n, steps)
+    if d <= 256:
+        ref = (O.plan_apply(A.cpu().numpy(), steps, np.eye(d)) if 15 in steps
+               else O.full_series(A.cpu().numpy(), OP.plan_reaches(steps)))
+        assert O.rel_fro(S, ref) <= 1e-11
+    assert st["gathers"] == 0 and st["launches"] == n * st["n_ops"]
+    assert st["products"] == OP.plan_products(steps, False)
+
+
+@pytest.mark.parametrize("n", [1, 4])
+def test_sharded_direct_residual(h, n):
+    d = 128
+    steps = [9, 1, 2]
+    An = inputs.random_matrix(d, 41, 0.7)
+    A = torch.from_numpy(An).cuda()
+    S, R, st = _sharded(h, A, steps, n, want_R=True, extra=P.NSERIES_SHARDED_DIRECT)
+    Sd, Rd = _dense(h, A, steps, want_R=True)
+    assert O.rel_fro(S, Sd) <= 1e-13 and O.rel_fro(R, Rd) <= 1e-12 and st["gathers"] == 0
+    assert O.rel_fro(S, O.full_series(An, OP.plan_reaches(steps))) <= 1e-11
+
+
+@pytest.mark.parametrize("d,n", [(200, 3), (100, 4), (1100, 8)])
+def test_sharded_direct_falls_back(h, d, n):
+    # non-uniform blocks or blocks of fewer than 32 / not a multiple of 32 rows: gathers
+    A = torch.from_numpy(inputs.random_matrix(d, 900 + d, 0.8)).cuda()
+    S, _, st = _sharded(h, A, [9, 9], n, extra=P.NSERIES_SHARDED_DIRECT)
+    Sd, _ = _dense(h, A, [9, 9])
+    assert O.rel_fro(S, Sd) <= 1e-13 and st["gathers"] >= 1
+
+
+def test_sharded_direct_config3():
+    # config 3 at full size in 8 row blocks of 512 rows, right factors read in place
+    hh = P.nseries_create(0)
+    try:
+        A, _, _ = inputs.cfg3(device="cuda")
+        S, _, st = _sharded(hh, A, [15, 15, 15], 8, extra=P.NSERIES_SHARDED_DIRECT)
+        Sd, _ = _dense(hh, A, [15, 15, 15])
+        assert O.rel_fro(S, Sd) <= 1e-12
+        assert st["products"] == 18 and st["gathers"] == 0
+    finally:
+        P.nseries_destroy(hh)
+
+
+@pytest.mark.parametrize("d,n,steps", [(256, 1, [9, 9]), (256, 4, [15, 15]), (512, 8, [15, 1, 5]),
+                                        (1024, 2, [2] * 6), (96, 3, [5, 1, 9])])
+def test_sharded_direct_peer_arena(d, n, steps):
+    # the cross-process NSERIES_SHARDED_DIRECT path on one GPU: a one-rank communicator owning all
+    # n shards, this rank's arena exported and "imported" (own entry), values' blocks in the arena,
+    # a one-int all-reduce barrier after every op; no gathers
+    hh = P.nseries_create(0)
+    try:
+        P.nseries_comm_init(hh, P.nseries_comm_unique_id(), 1, 0)
+        k = OP.plan_reaches(steps)
+        flags = _flags(steps, P.NSERIES_SHARDED_DIRECT)
+        plan = P.nseries_plan_finalize(steps, k, flags)
+        need = P.nseries_sharded_arena_bytes(d, n, n, k, plan, flags=flags)
+        P.nseries_peer_import(hh, [P.nseries_peer_export(hh, need)])
+        A = torch.from_numpy(inputs.random_matrix(d, 77 + d + n, 0.8)).cuda()
+        As = _shards(A, n)
+        Ss = [torch.full_like(a, float("nan")) for a in As]
+        for _ in range(2):                  # repeated evals reuse the arena (start barrier)
+            P.nseries_eval_sharded(hh, As, 0, n, d, k, plan=plan, S_shards=Ss, flags=flags)
+        torch.cuda.synchronize()
+        st = P.nseries_last_stats(hh)
+        S = torch.cat(Ss).cpu().numpy()
+        Sd, _ = _dense(hh, A, steps)
+        assert O.rel_fro(S, Sd) <= 1e-13 and st["gathers"] == 0, (d, n, steps)
+        ref = (O.plan_apply(A.cpu().numpy(), steps, np.eye(d)) if 15 in steps
+               else O.full_series(A.cpu().numpy(), k))
+        assert O.rel_fro(S, ref) <= 1e-11
+    finally:
+        P.nseries_destroy(hh)
+
+
+def test_sharded_direct_needs_import(hc, h):
+    # a communicator but no mapped arenas: NSERIES_SHARDED_DIRECT falls back to the gathers
+    d, n = 256, 4
+    A = torch.from_numpy(inputs.random_matrix(d, 5, 0.8)).cuda()
+    S, _, st = _sharded(hc, A, [9, 9], n, extra=P.NSERIES_SHARDED_DIRECT)
+    Sd, _ = _dense(h, A, [9, 9])
+    assert O.rel_fro(S, Sd) <= 1e-13 and st["gathers"] >= 1
 
 
 def test_sharded_rejects(h):

@@ -1,7 +1,9 @@
 """Host side of the multi-process row-sharded chain, world size 2
 over gloo on CPU: the 128-byte NCCL unique id is created by rank 0 through the library and
 shipped to rank 1 with torch.distributed (the plumbing bench/users run before
-nseries_comm_init), and every rank derives the same shard map from nseries_shard_rows."""
+nseries_comm_init), every rank derives the same shard map from nseries_shard_rows, and (for
+NSERIES_SHARDED_DIRECT across processes) every rank sizes the same arena with
+nseries_sharded_arena_bytes and receives all ranks' 64-byte IPC handles in rank order."""
 import os
 import socket
 
@@ -31,7 +33,13 @@ def _worker(rank, world, port, d, q):
     mine = P.nseries_shard_rows(d, world, rank)
     allb = [None] * world
     dist.all_gather_object(allb, mine)
-    q.put((rank, uid[0], allb, [P.nseries_shard_rows(d, world, s) for s in range(world)], have_uid))
+    plan = P.nseries_plan_build(10000, P.NSERIES_PLAN_AUTO, flags=P.NSERIES_ALLOW_APPROX)
+    arena = P.nseries_sharded_arena_bytes(d, world, 1, 10000, plan, flags=P.NSERIES_ALLOW_APPROX)
+    from paper_2602_11843_b200 import replicas
+    # stand-in for nseries_peer_export's handle (no GPU here): 64 rank-specific bytes
+    handles = replicas.exchange_blobs(bytes([rank + 1]) * 64, world)
+    q.put((rank, uid[0], allb, [P.nseries_shard_rows(d, world, s) for s in range(world)], have_uid,
+           arena, handles))
     dist.destroy_process_group()
 
 
@@ -47,7 +55,10 @@ def test_uid_exchange_and_shard_map(d):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, uid0, all0, map0, ok0), (r1, uid1, all1, map1, ok1) = res
+    (r0, uid0, all0, map0, ok0, ar0, hd0), (r1, uid1, all1, map1, ok1, ar1, hd1) = res
+    rows_max = max(n for _, n in map0)
+    assert ar0 == ar1 and ar0 > 0 and ar0 % (rows_max * d * 8) == 0   # (slots + A) row blocks
+    assert hd0 == hd1 == [bytes([1]) * 64, bytes([2]) * 64]
     assert len(uid0) == 128 and uid0 == uid1
     if ok0:
         assert any(uid0)                    # a real NCCL id, not zeros

@@ -1,6 +1,6 @@
 """Harness: row-sharded chain (NEXT-3) on one GPU, all row blocks local: ms per eval against
 the single-matrix engine, gathers per eval (env TIME_D, default 4096; plan x15^3 at 4096,
-AUTO k=10000 at 8192)."""
+AUTO k=10000 at 8192); each block count also with NSERIES_SHARDED_DIRECT (no gathers)."""
 import json
 import os
 import sys
@@ -46,4 +46,8 @@ for n in (1, 2, 8):
     out[f"sharded{n}_ms"] = round(ms, 3)
     out[f"sharded{n}_gathers"] = st["gathers"]
     out[f"sharded{n}_prefetched"] = st["gathers_prefetched"]
+    msd = timed(lambda: P.nseries_eval_sharded(h, As, 0, n, d, k, plan=plan, S_shards=Ss,
+                                               flags=fl | P.NSERIES_SHARDED_DIRECT), n_it)
+    out[f"sharded{n}_direct_ms"] = round(msd, 3)
+    out[f"sharded{n}_direct_gathers"] = P.nseries_last_stats(h)["gathers"]
 print(json.dumps(out))
