@@ -1,7 +1,8 @@
+// HISTORICAL (does not build against the current library, see tools/legacy/README.md).
 // Harness-only: per-op phase timing (clock64, CTA 0 thread 0) of the 4-CTA cluster small kernel
 // on an x9^2 plan at d = 64 (mainloop / epilogue / cluster barrier).
 #define NSERIES_SMALL_PROFILE
-#include "../paper_2602_11843_b200/csrc/plan_small.cu"
+#include "legacy/plan_small.cu"   // superseded kernels (moved out of the library in round 2)
 #include <cstdio>
 #include <vector>
 using namespace nseries;
