@@ -295,8 +295,10 @@ nseries_status nseries_shard_rows(int32_t d, int32_t nshards, int32_t shard, int
  *   (cudaIpcOpenMemHandle, P2P access enabled lazily), this rank's own entry is skipped.  Needs
  *   nseries_comm_init first with the same nranks.  Afterwards nseries_eval_sharded with
  *   NSERIES_SHARDED_DIRECT and a matching shard map reads right factors in place (the user's S
- *   / R blocks of peers are still gathered).  Handles mapped until nseries_destroy or the next
- *   import / a growing export. */
+ *   / R blocks of peers are still gathered).  Handles stay mapped until nseries_destroy or the
+ *   next import.  Every rank exports once, with the same size, before its first direct eval: a
+ *   later export that has to grow the arena frees the old one, which invalidates the peers'
+ *   mappings of it -- all ranks must then export and import again. */
 nseries_status nseries_sharded_arena_bytes(int32_t d, int32_t nshards, int32_t n_local, int64_t k,
                                           const nseries_plan* plan, uint32_t flags, int32_t want_R,
                                           uint64_t* bytes);
