@@ -64,6 +64,22 @@ def test_batched_f32(h, d, steps):
         assert O.rel_fro(S[b], ref) <= TOL32, (d, steps, b)
 
 
+@pytest.mark.parametrize("wpm", ["1", "2", "4"])
+@pytest.mark.parametrize("d", [17, 32])
+@pytest.mark.parametrize("steps", [[9, 9], [15, 15], [1, 2, 2], [5, 1, 9]])
+def test_batched_f32_warps_per_matrix(h, wpm, d, steps, monkeypatch):
+    # the warp-group kernel's tuning knob NSERIES_BATCHED_WPM (1, 2 = default, 4 warps per
+    # matrix): each variant tiles the fragments and finds the diagonal tiles differently
+    monkeypatch.setenv("NSERIES_BATCHED_WPM", wpm)
+    rng = np.random.default_rng(100 + d)
+    batch = 300                                  # > 148 x groups: every warp group takes several
+    Ab = (0.6 * rng.standard_normal((batch, d, d)) / np.sqrt(d)).astype(np.float32)
+    S = _batch(h, Ab, steps, torch.float32)
+    for b in (0, 1, 148, 149, batch - 1):
+        ref = _oracle(Ab[b].astype(np.float64), steps)
+        assert O.rel_fro(S[b], ref) <= TOL32, (wpm, d, steps, b)
+
+
 @pytest.mark.parametrize("d", [1, 4, 16, 17, 32])
 @pytest.mark.parametrize("steps", [[9, 9], [5, 5, 5], [15, 15], [1, 2, 2]])
 def test_batched_f64(h, d, steps):
