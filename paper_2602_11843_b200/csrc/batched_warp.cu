@@ -527,7 +527,10 @@ __device__ __forceinline__ void warp_op(const DevOp& op, float* ws, float* Sg, i
 // One CTA per SM holding up to 8 groups (one copy of the decoded op list per CTA); register
 // budgets: WPM 1 -> 255, 2 -> 128, 4 -> 64 per thread.
 template <int WPM>
-__global__ void __launch_bounds__(256 * WPM, 1)
+#ifndef NSERIES_BW_GROUPS
+#define NSERIES_BW_GROUPS 8   // warp groups (matrices) per CTA = per SM; the register budget follows
+#endif                        // (measured: 6 groups / 170 regs 255.6 us, 7 / 146 295 us, 8 / 128 254 us)
+__global__ void __launch_bounds__(32 * NSERIES_BW_GROUPS * WPM, 1)
 batched_warp_f32_kernel(const float* __restrict__ A, int64_t strideA, const float* const* __restrict__ A_ptrs,
                         float* __restrict__ S, int64_t strideS, float* const* __restrict__ S_ptrs, int batch,
                         int d, const __grid_constant__ WarpProgram prog, int* __restrict__ nonfinite) {
@@ -614,7 +617,7 @@ int launch_wpm(const void* A, int64_t strideA, const void* const* A_ptrs, void* 
                int* nonfinite) {
   const size_t per_group = (size_t)(prog.n_slots + 2) * kSlotF * sizeof(float);
   const size_t prog_bytes = 2 * (size_t)prog.n_ops * sizeof(DevOp);
-  const int groups = (int)std::min<size_t>(8, (227 * 1024 - prog_bytes) / per_group);
+  const int groups = (int)std::min<size_t>(NSERIES_BW_GROUPS, (227 * 1024 - prog_bytes) / per_group);
   if (groups < 1 || prog.n_slots + 2 > 60) return -1;   // uint16 float offsets
   const size_t smem = prog_bytes + groups * per_group;
   auto kern = batched_warp_f32_kernel<WPM>;
