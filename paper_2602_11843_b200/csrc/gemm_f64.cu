@@ -62,10 +62,12 @@ struct Cfg {
   static constexpr int kLdB = BN + 4;   // padded row of the B tile [BK][BN]
   static constexpr int kStageA = BM * kLdA, kStageB = BK * kLdB;
   static constexpr size_t kSmem = (size_t)STAGES * (kStageA + kStageB) * sizeof(double);
+  // 8 warps of 32x32 (64 accumulator registers): two CTAs per SM, 16 warps per SM
+  static constexpr int kMinBlocks = (kThreads == 256 && WM == 32 && WN == 32) ? 2 : 1;
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V2, bool SYM>
-__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::kThreads, 1)
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::kThreads, Cfg<BM, BN, BK, WM, WN, STAGES>::kMinBlocks)
 gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int d, EpiParams ep) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
   extern __shared__ __align__(16) double smem[];
@@ -423,6 +425,15 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   // (`profiles/r01_f64_tile_choice.txt`) 0.27 -> 0.46 of peak at d = 500, 0.72 -> 0.75 at 1024
   // (row blocks of the sharded chain: same rule on the block's M x d area)
   const bool small32 = !ep.sym && (double)M * d <= 1472.0 * 1472.0 && !(M == d && d > 704 && d <= 800);
+#ifdef NSERIES_F64_TILE_EXPERIMENTS
+  if (v2 && !ep.sym) {
+    if (force == 10) return launch_cfg_t<128, 64, 16, 32, 32, 3, true, false>(X, Y, d, ep, s);
+    if (force == 12) return launch_cfg_t<128, 128, 16, 32, 32, 4, true, false>(X, Y, d, ep, s);
+    if (force == 13) return launch_cfg_t<64, 128, 16, 32, 32, 3, true, false>(X, Y, d, ep, s);
+    if (force == 14) return launch_cfg_t<128, 128, 32, 32, 32, 3, true, false>(X, Y, d, ep, s);
+    if (force == 15) return launch_cfg_t<128, 64, 32, 32, 32, 2, true, false>(X, Y, d, ep, s);
+  }
+#endif
   if (force == 4 || (force == 0 && small32)) {
     if (ep.sym) return (int)cudaErrorInvalidValue;
     return v2 ? launch_cfg_t<32, 32, 16, 16, 16, 4, true, false>(X, Y, d, ep, s)
