@@ -432,8 +432,23 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
     if (force == 13) return launch_cfg_t<64, 128, 16, 32, 32, 3, true, false>(X, Y, d, ep, s);
     if (force == 14) return launch_cfg_t<128, 128, 32, 32, 32, 3, true, false>(X, Y, d, ep, s);
     if (force == 15) return launch_cfg_t<128, 64, 32, 32, 32, 2, true, false>(X, Y, d, ep, s);
+    if (force == 16) return launch_cfg_t<96, 80, 32, 24, 40, 3, true, false>(X, Y, d, ep, s);
+    if (force == 17) return launch_cfg_t<80, 96, 32, 40, 24, 3, true, false>(X, Y, d, ep, s);
+    if (force == 19) return launch_cfg_t<96, 80, 32, 48, 40, 3, true, false>(X, Y, d, ep, s);
   }
 #endif
+  // One wave of 96x80 tiles (8 warps of 24x40, BK 16, 4 stages, one CTA per SM) where a whole
+  // matrix cuts into <= 148 of them that fill >= 86% of the 148 SMs' tile area: d = 989..1040,
+  // i.e. config 2 (d = 1024: 11 x 13 = 143 tiles, fill 0.92).  The 32x32 tiles need 1.4 waves
+  // of 5 CTAs per SM there.  Measured (`profiles/r02_s7_cfg2_single_wave.txt`): plain product
+  // 0.758 -> 0.785 of the DMMA peak, x9^3 1.142 -> 1.107 ms, bit-identical results (every tile
+  // shape sums k in the same order).  NSERIES_F64_TILE = 20 forces it (harness only).
+  const double t1 = std::ceil(M / 96.0) * std::ceil(d / 80.0);
+  const bool wave1 = v2 && !ep.sym && M == d && t1 <= 148.0 && (double)M * d >= 0.86 * 148.0 * 96.0 * 80.0;
+  if (force == 20 || (force == 0 && wave1)) {
+    if (!v2 || ep.sym) return (int)cudaErrorInvalidValue;
+    return launch_cfg_t<96, 80, 16, 24, 40, 4, true, false>(X, Y, d, ep, s);
+  }
   if (force == 4 || (force == 0 && small32)) {
     if (ep.sym) return (int)cudaErrorInvalidValue;
     return v2 ? launch_cfg_t<32, 32, 16, 16, 16, 4, true, false>(X, Y, d, ep, s)

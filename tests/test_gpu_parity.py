@@ -143,7 +143,8 @@ def test_errors(h):
     assert e.value.status == 3
 
 
-@pytest.mark.parametrize("d", [1, 5, 64, 127, 300, 1536, 2048])
+# 990 / 1000 / 1024 / 1040: the one-wave 96x80 tiles (even d in 989..1040), ragged edges at 990 and 1000
+@pytest.mark.parametrize("d", [1, 5, 64, 127, 300, 990, 1000, 1024, 1040, 1536, 2048])
 def test_matmul_engine(h, d):
     rng = np.random.default_rng(d)
     X = rng.standard_normal((d, d))
@@ -186,6 +187,24 @@ def test_config2_probes(h, steps):
     V, _ = inputs.probe_block(A.shape[0], 1)
     S, _, _ = _run(h, A, steps)
     assert _probe_parity(S, A, steps, V, False) <= TOL64
+
+
+@pytest.mark.parametrize("steps", [[15, 15], [9, 9], [5, 1, 2]])
+def test_single_wave_tiles_d1000(h, steps):
+    # d = 1000 runs the 96x80 one-wave tiles (11 x 13 = 143 CTAs, ragged last row and column of
+    # tiles) through every epilogue form of these plans, S and R_out, on 16 probe columns
+    d = 1000
+    A = inputs.random_matrix(d, 41, 0.9)
+    V, _ = inputs.probe_block(d, 1)
+    S, R, _ = _run(h, A, steps, want_R=True)
+    approx = 15 in steps
+    assert _probe_parity(S, A, steps, V, approx) <= TOL64
+    # R_out = I - (I - A) S (PAPER.md residual identity), checked on the probes against the oracle's S V
+    k = OP.plan_reaches(steps)
+    SV = O.plan_apply(A, steps, V) if approx else O.series_sum(A, k, V)[0]
+    ref_R = V.astype(LD) - (SV - O.matvec(A, SV))
+    scale = float(np.sqrt(np.sum(np.asarray(SV, dtype=LD) ** 2)))
+    assert float(np.sqrt(np.sum((O.matvec(R, V) - ref_R) ** 2))) / scale <= 1e-12
 
 
 # configs 3 and 5 (d = 4096 / 8192, 16 probe columns against committed oracle goldens):
