@@ -43,6 +43,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
                "r"(valid ? 16 : 0));
 }
+// same, issued only when `on` (straight-line code: no branch around the copy)
+__device__ __forceinline__ void cp_async16_if(void* smem, const void* gmem, bool valid, bool on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16, %2;\n}\n"
+               ::"r"(smem_u32(smem)), "l"(gmem), "r"(valid ? 16 : 0), "r"((int)on));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
                "r"(valid ? 8 : 0));
@@ -158,6 +163,76 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
     }
   };
 
+#ifndef NSERIES_F64_NO_SPREAD
+  // The k-tile's copies spread over its k-steps (V2 only): part `k` of KK issues the chunks
+  // it = k ITA / KK .. (k+1) ITA / KK - 1 of each thread, so the address arithmetic and the
+  // LDGSTS issue between the DMMAs instead of in a block of their own at the top of the k-tile.
+  // Per-thread invariants are hoisted where a thread's chunks share one column (kThreads a multiple
+  // of the chunks per tile row): chunk `it` is then row r0 + it * rows-per-pass at a fixed column.
+  constexpr int kCA = BK / 2, kCB = BN / 2;                       // 16-byte chunks per tile row
+  // Measured (`profiles/r02_s7_f64_spread_loads.txt`): hoisting gains 1.7% on the 128x128 tiles and
+  // loses on the 64x64 tiles at two CTAs per SM (d = 2048: 0.915 -> 0.817), so only the former use it.
+  constexpr bool kHoist = BM == 128 && BN == 128;
+  constexpr bool kHoistA = kHoist && C::kThreads % kCA == 0, kHoistB = kHoist && C::kThreads % kCB == 0;
+  constexpr int kRA = C::kThreads / kCA, kRB = C::kThreads / kCB;   // tile rows per pass
+  const int a_r0 = tid / kCA, a_c = (tid % kCA) * 2, b_r0 = tid / kCB, b_c = (tid % kCB) * 2;
+  const double* const pA = X + (size_t)(m0 + a_r0) * d + a_c;      // + k0 per k-tile, + it kRA d per chunk
+  const int a_rows = M - m0 - a_r0;                                 // chunk `it` is inside A iff it kRA < a_rows
+  const bool b_col_ok = n0 + b_c < d;
+  const int sa_off = a_r0 * C::kLdA + a_c, sb_off = b_r0 * C::kLdB + b_c;
+  auto load_stage_part = [&](int stage, int kt, const double* Ykt, int part, int parts, bool on) {
+    const int k0 = kt * BK;
+    const double* const Yk = kHoist ? Ykt : y_rows(on ? k0 : 0);
+    double* a = sA + stage * C::kStageA;
+    double* b = sB + stage * C::kStageB;
+    constexpr int kChunksA = BM * BK / 2, kChunksB = BK * BN / 2;
+    constexpr int ITA = (kChunksA + C::kThreads - 1) / C::kThreads;
+    constexpr int ITB = (kChunksB + C::kThreads - 1) / C::kThreads;
+    if constexpr (kHoistA) {
+      const bool col_ok = k0 + a_c < d;
+#pragma unroll
+      for (int it = part * ITA / parts; it < (part + 1) * ITA / parts; ++it) {
+        if (kChunksA % C::kThreads == 0 || tid + it * C::kThreads < kChunksA) {
+          const bool ok = col_ok && it * kRA < a_rows;
+          cp_async16_if(a + sa_off + it * kRA * C::kLdA, ok ? pA + (size_t)(it * kRA) * d + k0 : X, ok, on);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int it = part * ITA / parts; it < (part + 1) * ITA / parts; ++it) {
+        const int q = tid + it * C::kThreads;
+        if (kChunksA % C::kThreads == 0 || q < kChunksA) {
+          int r = q / kCA, c = (q % kCA) * 2;
+          int gr = m0 + r, gc = k0 + c;
+          bool ok = gr < M && gc < d;
+          cp_async16_if(a + r * C::kLdA + c, ok ? X + (size_t)gr * d + gc : X, ok, on);
+        }
+      }
+    }
+    if constexpr (kHoistB) {
+      const double* const pB = Yk + (size_t)b_r0 * d + n0 + b_c;
+#pragma unroll
+      for (int it = part * ITB / parts; it < (part + 1) * ITB / parts; ++it) {
+        if (kChunksB % C::kThreads == 0 || tid + it * C::kThreads < kChunksB) {
+          const bool ok = b_col_ok && k0 + b_r0 + it * kRB < d;
+          cp_async16_if(b + sb_off + it * kRB * C::kLdB, ok ? pB + (size_t)(it * kRB) * d : Yk, ok, on);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int it = part * ITB / parts; it < (part + 1) * ITB / parts; ++it) {
+        const int q = tid + it * C::kThreads;
+        if (kChunksB % C::kThreads == 0 || q < kChunksB) {
+          int r = q / kCB, c = (q % kCB) * 2;
+          int gr = k0 + r, gc = n0 + c;
+          bool ok = gr < d && gc < d;
+          cp_async16_if(b + r * C::kLdB + c, ok ? Yk + (size_t)r * d + gc : Yk, ok, on);
+        }
+      }
+    }
+  };
+#endif
+
   double acc[C::kMI][C::kNI][2];
 #pragma unroll
   for (int i = 0; i < C::kMI; ++i)
@@ -192,9 +267,16 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
   load_frags(0, sA, sB, 0);
 
   for (int kt = 0; kt < KT; ++kt) {
-    {
-      // stage (kt-1) % STAGES was fully consumed before the barrier of iteration kt-1
-      const int nk = kt + STAGES - 1;
+    // stage (kt-1) % STAGES was fully consumed before the barrier of iteration kt-1
+    const int nk = kt + STAGES - 1;
+#ifndef NSERIES_F64_NO_SPREAD
+    constexpr bool kSpread = V2;   // -DNSERIES_F64_NO_SPREAD: the copies in one block per k-tile (A/B harness)
+#else
+    constexpr bool kSpread = false;
+#endif
+    // hoisted form: one row-block lookup per k-tile
+    const double* const Ynk = (kSpread && BM == 128 && BN == 128) ? y_rows(nk < KT ? nk * BK : 0) : Y;
+    if constexpr (!kSpread) {
       if (nk < KT) load_stage(nk % STAGES, nk);
       cp_async_commit();
     }
@@ -202,6 +284,12 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
     const double* b = sB + (kt % STAGES) * C::kStageB;
 #pragma unroll
     for (int k = 0; k < KK; ++k) {
+#ifndef NSERIES_F64_NO_SPREAD
+      if constexpr (kSpread) {
+        load_stage_part(nk % STAGES, nk, Ynk, k, KK, nk < KT);
+        if (k == KK - 1) cp_async_commit();
+      }
+#endif
       if (k == KK - 1) {
         NSERIES_SHAKE_POINT(kt);
         cp_async_wait<STAGES - 2>();   // tile kt+1 has landed
