@@ -45,7 +45,9 @@ def cases():
         ("tf32_matmul_d700", "matmul", 700, 1, None, "f32", False),
         ("tf32_x9x9_d1100", "single", 1100, 1, [9, 9], "f32", True),
         ("f64_x9p1x2_d300", "single", 300, 1, [9, 1, 2], "f64", True),
-        ("f64_x9x9_d1024", "single", 1024, 1, [9, 9], "f64", False),
+        ("f64_x9x9_d1024", "single", 1024, 1, [9, 9], "f64", False),     # one-wave 96x80 tiles
+        ("f64_x15p1x5_d1536", "single", 1536, 1, [15, 1, 5], "f64", True),  # 128x128 tiles, hoisted spread copies
+        ("f64_x9x9_d2048", "single", 2048, 1, [9, 9], "f64", False),     # 64x64 tiles, two CTAs per SM
     ]
 
 
