@@ -502,7 +502,7 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   // 128x128 tiles run one CTA per SM at ~0.935 with whole-wave quantisation; 64x64 tiles run
   // two CTAs per SM (~0.87 together, ~0.73 for a lone CTA) and, from two waves up, fill the
   // tail well enough that ~0.87 holds (d = 2048: 0.87 measured vs 0.79 for 128x128).
-  const double eb = 0.935 * tb / (std::ceil(tb / 148.0) * 148.0);
+  double eb = 0.935 * tb / (std::ceil(tb / 148.0) * 148.0);
   double es;
   if (ts >= 2 * 296) es = 0.87;
   else if (ts > 148) es = (ts / 148.0) / (2.0 * std::ceil(ts / 296.0) / 0.87);
@@ -512,7 +512,22 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
   // except where 64x64 tiles fill exactly one wave (d ~ 768: 144 tiles): measured
   // (`profiles/r01_f64_tile_choice.txt`) 0.27 -> 0.46 of peak at d = 500, 0.72 -> 0.75 at 1024
   // (row blocks of the sharded chain: same rule on the block's M x d area)
-  const bool small32 = !ep.sym && (double)M * d <= 1472.0 * 1472.0 && !(M == d && d > 704 && d <= 800);
+  bool small32 = !ep.sym && (double)M * d <= 1472.0 * 1472.0 && !(M == d && d > 704 && d <= 800);
+  // Whole even-d matrices (the spread-copy kernels, session 7) choose by a model refitted to
+  // `profiles/r02_s7_tile_model.txt`: 128x128 at (0.90 + 0.065 d/3072, capped 0.965) x whole-wave
+  // fill; 64x64 as pairs of CTAs per SM -- an SM with c = ceil(tiles/148) tiles runs floor(c/2)
+  // pairs at 0.92 and a last lone tile at 0.75 (within 0.03 of all 15 measured sizes; +0.025
+  // from ~3.5 waves up, where dynamic scheduling smooths the tail); 32x32 at
+  // min(0.73, 0.00116 d - 0.23) up to d = 1472.  Sharded row blocks, symmetric mode and odd d
+  // keep the rules above.
+  if (v2 && !ep.sym && M == d) {
+    eb = std::min(0.965, 0.90 + 0.065 * d / 3072.0) * tb / (std::ceil(tb / 148.0) * 148.0);
+    const double c = std::ceil(ts / 148.0);
+    const double t = std::floor(c / 2.0) * (2.0 / 0.92) + (std::fmod(c, 2.0) > 0.5 ? 1.0 / 0.75 : 0.0);
+    es = (ts / 148.0) / t + (ts >= 1000.0 ? 0.025 : 0.0);
+    const double e32 = d <= 1472 ? std::min(0.73, 0.00116 * d - 0.23) : 0.0;
+    small32 = e32 >= std::max(es, eb);
+  }
 #ifdef NSERIES_F64_TILE_EXPERIMENTS
   if (v2 && !ep.sym) {
     if (force == 10) return launch_cfg_t<128, 64, 16, 32, 32, 3, true, false>(X, Y, d, ep, s);
