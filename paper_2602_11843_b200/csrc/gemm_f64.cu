@@ -172,8 +172,12 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
   constexpr int kCA = BK / 2, kCB = BN / 2;                       // 16-byte chunks per tile row
   // Measured (`profiles/r02_s7_f64_spread_loads.txt`): hoisting gains 1.7% on the 128x128 tiles and
   // loses on the 64x64 tiles at two CTAs per SM (d = 2048: 0.915 -> 0.817), so only the former use it.
-  constexpr bool kHoist = BM == 128 && BN == 128;
-  constexpr bool kHoistA = kHoist && C::kThreads % kCA == 0, kHoistB = kHoist && C::kThreads % kCB == 0;
+#ifndef NSERIES_F64_HOIST64
+#define NSERIES_F64_HOIST64 0   // harness: 1 = hoist A's, 2 = B's, 3 = both on the 64x64 tiles
+#endif
+  constexpr int kHoistSel = (BM == 128 && BN == 128) ? 3 : (BM == 64 && BN == 64) ? NSERIES_F64_HOIST64 : 0;
+  constexpr bool kHoist = kHoistSel != 0;
+  constexpr bool kHoistA = (kHoistSel & 1) && C::kThreads % kCA == 0, kHoistB = (kHoistSel & 2) && C::kThreads % kCB == 0;
   constexpr int kRA = C::kThreads / kCA, kRB = C::kThreads / kCB;   // tile rows per pass
   const int a_r0 = tid / kCA, a_c = (tid % kCA) * 2, b_r0 = tid / kCB, b_c = (tid % kCB) * 2;
   const double* const pA = X + (size_t)(m0 + a_r0) * d + a_c;      // + k0 per k-tile, + it kRA d per chunk
@@ -272,10 +276,10 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #ifndef NSERIES_F64_NO_SPREAD
     constexpr bool kSpread = V2;   // -DNSERIES_F64_NO_SPREAD: the copies in one block per k-tile (A/B harness)
 #else
-    constexpr bool kSpread = false;
+    constexpr bool kSpread = false, kHoist = false;
 #endif
     // hoisted form: one row-block lookup per k-tile
-    const double* const Ynk = (kSpread && BM == 128 && BN == 128) ? y_rows(nk < KT ? nk * BK : 0) : Y;
+    const double* const Ynk = (kSpread && kHoist) ? y_rows(nk < KT ? nk * BK : 0) : Y;
     if constexpr (!kSpread) {
       if (nk < KT) load_stage(nk % STAGES, nk);
       cp_async_commit();
