@@ -341,7 +341,7 @@ def run_native(args):
 
     roof = {"bound": "tensor", "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": tflops / FP64_PEAK_TFLOPS, "traffic": _traffic(),
-            "kernel": "gemm_f64_kernel<128,128,32,64,32,3> (DMMA.8x8x4)",
+            "kernel": "gemm_f64_kernel<128,128,16,64,32,4> (DMMA.8x8x4)",
             "algorithmic_flops_per_launch": flop_per_product,
             "note": "achieved = 2 d^3 per GEMM launch / average launch duration over the timed region "
                     "(every launch in the step is this kernel); peak " + FP64_PEAK_SOURCE}

@@ -539,6 +539,7 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
     if (force == 13) return launch_cfg_t<64, 128, 16, 32, 32, 3, true, false>(X, Y, d, ep, s);
     if (force == 14) return launch_cfg_t<128, 128, 32, 32, 32, 3, true, false>(X, Y, d, ep, s);
     if (force == 15) return launch_cfg_t<128, 64, 32, 32, 32, 2, true, false>(X, Y, d, ep, s);
+    if (force == 22) return launch_cfg_t<128, 128, 16, 64, 32, 6, true, false>(X, Y, d, ep, s);
     if (force == 16) return launch_cfg_t<96, 80, 32, 24, 40, 3, true, false>(X, Y, d, ep, s);
     if (force == 17) return launch_cfg_t<80, 96, 32, 40, 24, 3, true, false>(X, Y, d, ep, s);
     if (force == 19) return launch_cfg_t<96, 80, 32, 48, 40, 3, true, false>(X, Y, d, ep, s);
@@ -561,9 +562,14 @@ int launch_gemm_f64(const double* X, const double* Y, int d, const EpiParams& ep
     return v2 ? launch_cfg_t<32, 32, 16, 16, 16, 4, true, false>(X, Y, d, ep, s)
               : launch_cfg_t<32, 32, 16, 16, 16, 4, false, false>(X, Y, d, ep, s);
   }
-  if (force == 1 || (force == 0 && eb >= es)) {
-    return v2 ? launch_cfg<128, 128, 32, 64, 32, 3, true>(X, Y, d, ep, s)
-              : launch_cfg<128, 128, 32, 64, 32, 3, false>(X, Y, d, ep, s);
+  if (force == 1 || force == 2 || (force == 0 && eb >= es)) {
+    // BK 16 / 4 stages since the copies are spread over the k-steps (session 7: x15^3 70.01 ->
+    // 69.64 ms against BK 32 / 3 stages, 6 stages no better); NSERIES_F64_TILE = 2 forces the old shape
+    if (force == 2)
+      return v2 ? launch_cfg<128, 128, 32, 64, 32, 3, true>(X, Y, d, ep, s)
+                : launch_cfg<128, 128, 32, 64, 32, 3, false>(X, Y, d, ep, s);
+    return v2 ? launch_cfg<128, 128, 16, 64, 32, 4, true>(X, Y, d, ep, s)
+              : launch_cfg<128, 128, 16, 64, 32, 4, false>(X, Y, d, ep, s);
   }
   return v2 ? launch_cfg<64, 64, kBK64, 32, 16, kST64, true>(X, Y, d, ep, s)
             : launch_cfg<64, 64, kBK64, 32, 16, kST64, false>(X, Y, d, ep, s);
