@@ -175,7 +175,11 @@ gemm_f64_kernel(const double* __restrict__ X, const double* __restrict__ Y, int 
 #ifndef NSERIES_F64_HOIST64
 #define NSERIES_F64_HOIST64 0   // harness: 1 = hoist A's, 2 = B's, 3 = both on the 64x64 tiles
 #endif
-  constexpr int kHoistSel = (BM == 128 && BN == 128) ? 3 : (BM == 64 && BN == 64) ? NSERIES_F64_HOIST64 : 0;
+#ifndef NSERIES_F64_HOIST96
+#define NSERIES_F64_HOIST96 0   // harness: 1 = hoist A's on the 96x80 tiles (B's 40 chunks per row do not divide 256)
+#endif
+  constexpr int kHoistSel = (BM == 128 && BN == 128) ? 3 : (BM == 64 && BN == 64) ? NSERIES_F64_HOIST64
+                            : (BM == 96 && BN == 80) ? NSERIES_F64_HOIST96 : 0;
   constexpr bool kHoist = kHoistSel != 0;
   constexpr bool kHoistA = (kHoistSel & 1) && C::kThreads % kCA == 0, kHoistB = (kHoistSel & 2) && C::kThreads % kCB == 0;
   constexpr int kRA = C::kThreads / kCA, kRB = C::kThreads / kCB;   // tile rows per pass
